@@ -1,0 +1,177 @@
+/*
+ * driftcast_gpu.h -- C ABI of the B200-native IEWPF hot path (libdriftcast_gpu.so).
+ *
+ * Drop-in boundary for the reference's C++ operator surface (namespace driftcast,
+ * proj/include/driftcast/{grid,field,rng,state,swe,stochastic}.hpp). Every entry point is batched over the
+ * ensemble held by one context (one context per process / GPU); all calls are
+ * stream-ordered and asynchronous unless stated. Plain pointers and sizes only.
+ *
+ * Host arrays use the reference layout: Field2D row-major, j fastest, element (j,k) at
+ * k*nx+j (field.hpp:10-11,48-50); member-major for ensemble arrays. Device layout is
+ * private (members batched along y, rows padded to 128 B).
+ *
+ * Errors: calls return a dc_status; the reference's exceptions map to codes
+ * (std::invalid_argument -> DC_EINVAL, DryCellError -> DC_EDRY, "non-finite value after
+ * substep" -> DC_ENONFINITE, "substep count exploded" -> DC_ERUNAWAY). Device-side
+ * failures surface at the next synchronising call (dc_sync, downloads, diagnostics)
+ * with the reference's message shapes via dc_last_error. include/driftcast_gpu.hpp maps
+ * codes back to the reference exception types.
+ */
+#ifndef DRIFTCAST_GPU_H
+#define DRIFTCAST_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum dc_status {
+    DC_OK = 0,
+    DC_EINVAL = 1,     /* std::invalid_argument */
+    DC_EDRY = 2,       /* DryCellError (swe.hpp:32-34) */
+    DC_ENONFINITE = 3, /* std::runtime_error "model_step: non-finite value after substep k" */
+    DC_ERUNAWAY = 4,   /* std::runtime_error "model_step: substep count exploded" */
+    DC_EALIGN = 5,     /* apply_q_half_T: observation not co-located */
+    DC_ECUDA = 6,      /* CUDA runtime failure */
+    DC_ESTATE = 7      /* API misuse (bad member index, wrong call order) */
+} dc_status;
+
+/* Parameter block: ModelGrid + PhysParams + SchemeParams + ErrorParams + seed. */
+typedef struct dc_config {
+    int32_t nx, ny;                 /* ModelGrid (grid.hpp:11-29) */
+    double dx, dy;
+    double g, f, h_eq;              /* PhysParams (grid.hpp:31-42) */
+    double courant, limiter_theta;  /* SchemeParams (swe.hpp:16-30) */
+    double model_dt;
+    double q0, l0;                  /* ErrorParams (stochastic.hpp:17-32) */
+    int32_t c_omega;                /* CoarseGrid factor (grid.hpp:74-96), odd, divides nx,ny */
+    int32_t c_soar;                 /* must be 2 (stochastic.hpp:20,54) */
+    uint64_t seed;                  /* experiment master seed (rng.hpp:35-40) */
+    int32_t exact_fp;               /* 1: IEEE, no FMA contraction (bitwise reference parity);
+                                       0: FMA contraction in the stencil (tolerance parity) */
+    int32_t reserved;
+} dc_config;
+
+/* Noise sources for model error / filter draws. */
+typedef enum dc_noise_mode {
+    DC_NOISE_PHILOX = 0,   /* counter-based Philox4x32-10 keyed by stream_seed(seed,tag,member) */
+    DC_NOISE_INJECTED = 1  /* host-given offsets + xi (e.g. from the reference NoiseStream) */
+} dc_noise_mode;
+
+/* Observation record at t^n (SPEC.md ObservationRecord): location + observed transports. */
+typedef struct dc_obs {
+    double x, y;       /* m, periodic */
+    double y_hu, y_hv; /* m^2/s */
+} dc_obs;
+
+/* Per-particle IEWPF diagnostics (SPEC.md ParticleDiagnostics). */
+typedef struct dc_particle_diag {
+    double c, phi, gamma, zeta, alpha;
+} dc_particle_diag;
+
+typedef struct dc_ctx dc_ctx;
+
+/* ---- lifetime ------------------------------------------------------------------ */
+/* Create a context holding n_members particles whose global ids are
+ * member_base .. member_base+n_members-1 (RNG stream identity uses the global id,
+ * rng.hpp:35-40). stream: a cudaStream_t to run on, or NULL for an owned stream.
+ * Replaces: Stepper ctor (swe.hpp:194-207) + the ensemble container. */
+dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base,
+                    int32_t device, void* stream, dc_ctx** out);
+dc_status dc_destroy(dc_ctx* ctx);
+dc_status dc_sync(dc_ctx* ctx); /* waits; surfaces device errors */
+const char* dc_last_error(dc_ctx* ctx, int32_t* member, int32_t* j, int32_t* k,
+                          int32_t* substep);
+const char* dc_version(void);
+
+/* ---- state I/O (OceanState, state.hpp:18-31) ---------------------------------- */
+dc_status dc_upload_member(dc_ctx* ctx, int32_t m, const float* eta, const float* hu,
+                           const float* hv, double t);
+dc_status dc_download_member(dc_ctx* ctx, int32_t m, float* eta, float* hu, float* hv,
+                             double* t);
+/* all members, member-major [n_members][ny][nx]; t may be NULL */
+dc_status dc_upload_all(dc_ctx* ctx, const float* eta, const float* hu, const float* hv,
+                        const double* t);
+dc_status dc_download_all(dc_ctx* ctx, float* eta, float* hu, float* hv, double* t);
+
+/* ---- model operator M (swe.hpp) ----------------------------------------------- */
+/* init_double_jet (swe.hpp:459-500), default JetParams, broadcast to every member. */
+dc_status dc_init_double_jet(dc_ctx* ctx);
+/* n_steps x Stepper::model_step (swe.hpp:244-259) on every member. */
+dc_status dc_step(dc_ctx* ctx, int32_t n_steps);
+/* Stepper::flux_rhs (swe.hpp:229-239) of member m (synchronous; host outputs). */
+dc_status dc_flux_rhs(dc_ctx* ctx, int32_t m, float* d_eta, float* d_hu, float* d_hv);
+/* Stepper::cfl_dt (swe.hpp:212-226) of every member (synchronous; host output). */
+dc_status dc_cfl_dt(dc_ctx* ctx, double* dt_out);
+/* substep counts of the last model step per member (synchronous). */
+dc_status dc_substeps(dc_ctx* ctx, int32_t* out);
+
+/* ---- model error (stochastic.hpp) --------------------------------------------- */
+/* perturb_state (stochastic.hpp:164-173) on every member. PHILOX: offsets and xi drawn
+ * from (seed, model_error, member) at the context's draw counter, which then advances.
+ * INJECTED: offsets [n_members][2] and xi [n_members][nxc*nyc] (b-outer, a-inner). */
+dc_status dc_perturb(dc_ctx* ctx, int32_t mode, const int32_t* offsets, const double* xi);
+/* add_q_half (stochastic.hpp:144-160) of host coarse fields on per-member offsets. */
+dc_status dc_add_q_half(dc_ctx* ctx, const int32_t* offsets, const double* coarse,
+                        double scale);
+dc_status dc_get_draw_counter(dc_ctx* ctx, uint64_t* model_error_draw);
+dc_status dc_set_draw_counter(dc_ctx* ctx, uint64_t model_error_draw);
+
+/* ---- observation system ------------------------------------- */
+/* innovation of every member at n_obs observations -> d[m][o][2]
+ * (synchronous, host output). */
+dc_status dc_innovations(dc_ctx* ctx, const dc_obs* obs, int32_t n_obs, double* d_out);
+/* observe_mooring without noise on member m -> y[o][2] (synchronous). */
+dc_status dc_observe_mooring(dc_ctx* ctx, int32_t m, const double* xy, int32_t n,
+                             double* y_out);
+/* Per-member drifter copies: positions [n_members][n_d][2]. */
+dc_status dc_drifters_set(dc_ctx* ctx, const double* pos, int32_t n_d);
+/* advect_drifters, forward Euler at the containing cell. */
+dc_status dc_drifters_advect(dc_ctx* ctx, double dt);
+/* positions and winding counts [n_members][n_d][2] (synchronous). */
+dc_status dc_drifters_get(dc_ctx* ctx, double* pos, int32_t* wind);
+
+/* ---- IEWPF --------------------------------------------------- */
+/* precompute_S on the host in fp64: HQH^T and S = (HQH^T+R)^-1,
+ * row-major 2x2. Context-free. */
+dc_status dc_precompute_S(const dc_config* cfg, double r_hu, double r_hv, double* hqht,
+                          double* S);
+/* precompute_local_svd: 49x49 block and U Sigma^{1/2} (row-major).
+ * Context-free; symmetric eigen-decomposition (the block is symmetric PSD). */
+dc_status dc_precompute_local_svd(const dc_config* cfg, const double* S, double* block,
+                                  double* usig);
+/* Stages 1-3 for the context's particles: innovations, pulls (+phi, c), perpendicular
+ * pair (gamma, zeta). Writes this slice's (c_i, zeta_i) pairs to cz_out
+ * ([n_members][2], DEVICE pointer if cz_out_is_device, else host, synchronous).
+ * cycle selects the filter-stream draw. n_total: global ensemble size N_e. */
+dc_status dc_iewpf_begin(dc_ctx* ctx, const dc_obs* obs, int32_t n_obs, const double* S,
+                         const double* usig, uint64_t cycle, int32_t n_total, void* cz_out,
+                         int32_t cz_out_is_device);
+/* Stages 4-6 given ALL particles' (c_i, zeta_i) ([n_total][2], device pointer if
+ * cz_is_device): barrier scalars, alpha, P^{1/2} posterior update. */
+dc_status dc_iewpf_finish(dc_ctx* ctx, const void* cz_all, int32_t cz_is_device);
+/* Single-context convenience: begin + finish without a collective (n_total = n_members). */
+dc_status dc_iewpf_assimilate(dc_ctx* ctx, const dc_obs* obs, int32_t n_obs, const double* S,
+                              const double* usig, uint64_t cycle);
+/* Diagnostics of the last analysis (synchronous): per particle + (w_target, beta). */
+dc_status dc_iewpf_diagnostics(dc_ctx* ctx, dc_particle_diag* per_member, double* w_beta);
+
+/* ---- one data-assimilation cycle ----------------------------- */
+/* n_steps model steps; model error (PHILOX) after each but the last; drifters advected
+ * by model_dt before each step when drifters are set; then the IEWPF analysis
+ * (single-context). Stream-ordered, no host sync inside. */
+dc_status dc_da_cycle(dc_ctx* ctx, int32_t n_steps, const dc_obs* obs, int32_t n_obs,
+                      const double* S, const double* usig, uint64_t cycle);
+
+/* ---- instrumentation ------------------------------------------------------------ */
+/* number of kernels this context has launched (host-side counter). */
+int64_t dc_kernel_launches(dc_ctx* ctx);
+/* device pointers (for external collectives / profiling); may be NULL. */
+void* dc_stream(dc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DRIFTCAST_GPU_H */

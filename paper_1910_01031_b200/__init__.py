@@ -1,0 +1,11 @@
+"""B200-native IEWPF hot path (arXiv 1910.01031): ensemble shallow-water forecast,
+model-error perturbation, two-stage IEWPF analysis and drifter advection as sm_100a
+CUDA kernels behind the C ABI in include/driftcast_gpu.h.
+
+The compute lives in libdriftcast_gpu.so (C++/CUDA). This package only binds it.
+"""
+from ._lib import DcError, load  # noqa: F401
+from .ensemble import Config, Ensemble, obs_array, precompute_S, precompute_local_svd  # noqa: F401
+
+__all__ = ["Config", "Ensemble", "DcError", "load", "obs_array", "precompute_S",
+           "precompute_local_svd"]

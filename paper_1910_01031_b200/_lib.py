@@ -1,0 +1,124 @@
+"""ctypes binding of the C ABI in include/driftcast_gpu.h (libdriftcast_gpu.so).
+
+This is the Python face of the drop-in boundary used by the tests and bench.py; the
+library itself is C++/CUDA. There is no CPU fallback: if the shared library is missing
+or no GPU is present, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdriftcast_gpu.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "driftcast_gpu.h")
+
+DC_OK, DC_EINVAL, DC_EDRY, DC_ENONFINITE, DC_ERUNAWAY, DC_EALIGN, DC_ECUDA, DC_ESTATE = range(8)
+DC_NOISE_PHILOX, DC_NOISE_INJECTED = 0, 1
+
+STATUS_NAMES = {
+    DC_OK: "DC_OK", DC_EINVAL: "DC_EINVAL", DC_EDRY: "DC_EDRY", DC_ENONFINITE: "DC_ENONFINITE",
+    DC_ERUNAWAY: "DC_ERUNAWAY", DC_EALIGN: "DC_EALIGN", DC_ECUDA: "DC_ECUDA",
+    DC_ESTATE: "DC_ESTATE",
+}
+
+
+class DcConfig(C.Structure):
+    """dc_config (include/driftcast_gpu.h)."""
+
+    _fields_ = [
+        ("nx", C.c_int32), ("ny", C.c_int32), ("dx", C.c_double), ("dy", C.c_double),
+        ("g", C.c_double), ("f", C.c_double), ("h_eq", C.c_double),
+        ("courant", C.c_double), ("limiter_theta", C.c_double), ("model_dt", C.c_double),
+        ("q0", C.c_double), ("l0", C.c_double), ("c_omega", C.c_int32), ("c_soar", C.c_int32),
+        ("seed", C.c_uint64), ("exact_fp", C.c_int32), ("reserved", C.c_int32),
+    ]
+
+
+class DcObs(C.Structure):
+    _fields_ = [("x", C.c_double), ("y", C.c_double), ("y_hu", C.c_double), ("y_hv", C.c_double)]
+
+
+class DcParticleDiag(C.Structure):
+    _fields_ = [("c", C.c_double), ("phi", C.c_double), ("gamma", C.c_double),
+                ("zeta", C.c_double), ("alpha", C.c_double)]
+
+
+# Every symbol the header declares (checked by tests/test_cabi.py without a GPU).
+EXPORTS = [
+    "dc_create", "dc_destroy", "dc_sync", "dc_last_error", "dc_version",
+    "dc_upload_member", "dc_download_member", "dc_upload_all", "dc_download_all",
+    "dc_init_double_jet", "dc_step", "dc_flux_rhs", "dc_cfl_dt", "dc_substeps",
+    "dc_perturb", "dc_add_q_half", "dc_get_draw_counter", "dc_set_draw_counter",
+    "dc_innovations", "dc_observe_mooring", "dc_drifters_set", "dc_drifters_advect",
+    "dc_drifters_get", "dc_precompute_S", "dc_precompute_local_svd", "dc_iewpf_begin",
+    "dc_iewpf_finish", "dc_iewpf_assimilate", "dc_iewpf_diagnostics", "dc_da_cycle",
+    "dc_kernel_launches", "dc_stream",
+]
+
+
+class DcError(RuntimeError):
+    def __init__(self, status: int, message: str, member=-1, j=-1, k=-1, substep=-1):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+        self.member, self.j, self.k, self.substep = member, j, k, substep
+
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load libdriftcast_gpu.so and declare every signature. Raises if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the CUDA library is required; there is no CPU fallback)")
+    L = C.CDLL(path)
+    vp, dp, fp, ip = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_float), C.POINTER(C.c_int32)
+    cfgp = C.POINTER(DcConfig)
+    obsp = C.POINTER(DcObs)
+    st = C.c_int
+    sigs = {
+        "dc_create": (st, [cfgp, C.c_int32, C.c_int64, C.c_int32, vp, C.POINTER(vp)]),
+        "dc_destroy": (st, [vp]),
+        "dc_sync": (st, [vp]),
+        "dc_last_error": (C.c_char_p, [vp, ip, ip, ip, ip]),
+        "dc_version": (C.c_char_p, []),
+        "dc_upload_member": (st, [vp, C.c_int32, fp, fp, fp, C.c_double]),
+        "dc_download_member": (st, [vp, C.c_int32, fp, fp, fp, dp]),
+        "dc_upload_all": (st, [vp, fp, fp, fp, dp]),
+        "dc_download_all": (st, [vp, fp, fp, fp, dp]),
+        "dc_init_double_jet": (st, [vp]),
+        "dc_step": (st, [vp, C.c_int32]),
+        "dc_flux_rhs": (st, [vp, C.c_int32, fp, fp, fp]),
+        "dc_cfl_dt": (st, [vp, dp]),
+        "dc_substeps": (st, [vp, ip]),
+        "dc_perturb": (st, [vp, C.c_int32, ip, dp]),
+        "dc_add_q_half": (st, [vp, ip, dp, C.c_double]),
+        "dc_get_draw_counter": (st, [vp, C.POINTER(C.c_uint64)]),
+        "dc_set_draw_counter": (st, [vp, C.c_uint64]),
+        "dc_innovations": (st, [vp, obsp, C.c_int32, dp]),
+        "dc_observe_mooring": (st, [vp, C.c_int32, dp, C.c_int32, dp]),
+        "dc_drifters_set": (st, [vp, dp, C.c_int32]),
+        "dc_drifters_advect": (st, [vp, C.c_double]),
+        "dc_drifters_get": (st, [vp, dp, ip]),
+        "dc_precompute_S": (st, [cfgp, C.c_double, C.c_double, dp, dp]),
+        "dc_precompute_local_svd": (st, [cfgp, dp, dp, dp]),
+        "dc_iewpf_begin": (st, [vp, obsp, C.c_int32, dp, dp, C.c_uint64, C.c_int32, vp, C.c_int32]),
+        "dc_iewpf_finish": (st, [vp, vp, C.c_int32]),
+        "dc_iewpf_assimilate": (st, [vp, obsp, C.c_int32, dp, dp, C.c_uint64]),
+        "dc_iewpf_diagnostics": (st, [vp, C.POINTER(DcParticleDiag), dp]),
+        "dc_da_cycle": (st, [vp, C.c_int32, obsp, C.c_int32, dp, dp, C.c_uint64]),
+        "dc_kernel_launches": (C.c_int64, [vp]),
+        "dc_stream": (vp, [vp]),
+    }
+    for name, (res, args) in sigs.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L

@@ -1,0 +1,682 @@
+// api.cu -- the C ABI (include/driftcast_gpu.h): ensemble context, device memory,
+// the device-side substep loop as a CUDA graph with a while-node, error surfacing.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dc_internal.h"
+#include "detmath.cuh"
+#include "iewpf_host.h"
+
+using namespace dcg;
+
+struct dc_ctx {
+    dc_config cfg{};
+    int M = 0;
+    int64_t base = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool exact = true;
+    SweParams sp{};
+    ErrParams ep{};
+    int nr = 0;
+    size_t field_elems = 0;
+    float* f[6] = {nullptr};  // eta, hu, hv, stage eta, stage hu, stage hv
+    StepCtl ctl{};
+    void* ctl_mem = nullptr;
+    unsigned long long* substep_iters = nullptr; // device counter (graph path)
+    double* xi = nullptr;
+    double* corr = nullptr;
+    int* offs = nullptr;
+    uint64_t me_draw = 0;
+    // flux_rhs scratch (one member)
+    float* rhs = nullptr;
+    unsigned long long* gmax = nullptr;
+    // graph of one model step
+    cudaGraphExec_t step_exec = nullptr;
+    bool use_graph = true;
+    int64_t launches = 0;
+    int last_max_sub = 8;
+    // IEWPF / observation / drifter state
+    IewpfBuffers iw{};
+    // error reporting
+    std::string err;
+    int em = -1, ej = -1, ek = -1, esub = -1;
+};
+
+namespace {
+
+const char* kVersion = "driftcast-b200 0.1 (sm_100a)";
+
+dc_status set_err(dc_ctx* c, dc_status st, const std::string& msg, int m = -1, int j = -1,
+                  int k = -1, int sub = -1) {
+    if (c) {
+        c->err = msg;
+        c->em = m;
+        c->ej = j;
+        c->ek = k;
+        c->esub = sub;
+    }
+    return st;
+}
+
+#define CU(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return set_err(ctx, DC_ECUDA, std::string("CUDA: ") + cudaGetErrorString(e_) + \
+                                              " at " #call);                               \
+    } while (0)
+
+dc_status validate(const dc_config* c, std::string* why) {
+    if (c->nx < 8 || c->ny < 8) return *why = "ModelGrid: need nx,ny >= 8", DC_EINVAL;
+    if (!(c->dx > 0.0) || !(c->dy > 0.0)) return *why = "ModelGrid: need dx,dy > 0", DC_EINVAL;
+    if (!(c->g > 0.0)) return *why = "PhysParams: g must be > 0", DC_EINVAL;
+    if (!(c->h_eq > 0.0)) return *why = "PhysParams: h_eq must be > 0", DC_EINVAL;
+    if (c->f == 0.0) return *why = "PhysParams: f must be nonzero", DC_EINVAL;
+    if (!(c->courant > 0.0 && c->courant < 1.0))
+        return *why = "SchemeParams: courant in (0,1)", DC_EINVAL;
+    if (!(c->limiter_theta >= 1.0 && c->limiter_theta <= 2.0))
+        return *why = "SchemeParams: limiter_theta in [1,2]", DC_EINVAL;
+    if (!(c->model_dt > 0.0)) return *why = "SchemeParams: model_dt > 0", DC_EINVAL;
+    if (c->q0 < 0.0) return *why = "ErrorParams: q0 must be >= 0", DC_EINVAL;
+    if (c->q0 > 0.0 && !(c->l0 > 0.0)) return *why = "ErrorParams: l0 must be > 0", DC_EINVAL;
+    if (c->c_omega <= 0 || c->c_omega % 2 == 0)
+        return *why = "CoarseGrid: coarsening factor must be odd and positive", DC_EINVAL;
+    if (c->nx % c->c_omega != 0 || c->ny % c->c_omega != 0)
+        return *why = "CoarseGrid: c_omega must divide nx and ny", DC_EINVAL;
+    if (c->c_soar != 2) return *why = "ErrorParams: c_soar is fixed at 2", DC_EINVAL;
+    return DC_OK;
+}
+
+double soar_kernel(double dist, double q0, double l0) { // stochastic.hpp:43-45
+    return q0 * (1.0 + dist / l0) * std::exp(-dist / l0);
+}
+
+void derive_params(dc_ctx* c) {
+    const dc_config& g = c->cfg;
+    SweParams& P = c->sp;
+    P.nx = g.nx;
+    P.ny = g.ny;
+    P.pitch = (g.nx + 31) / 32 * 32;
+    P.M = c->M;
+    P.strips = (g.ny + 31) / 32;
+    P.by = (g.ny + P.strips - 1) / P.strips;
+    P.strips = (g.ny + P.by - 1) / P.by;
+    P.H = static_cast<float>(g.h_eq);
+    P.g = static_cast<float>(g.g);
+    P.theta = static_cast<float>(g.limiter_theta);
+    P.cf_x = static_cast<float>(g.f * g.dx / (2.0 * g.h_eq));
+    P.cf_y = static_cast<float>(g.f * g.dy / (2.0 * g.h_eq));
+    P.inv_g = 1.0f / P.g;
+    P.idx = static_cast<float>(1.0 / g.dx);
+    P.idy = static_cast<float>(1.0 / g.dy);
+    P.fH = static_cast<float>(g.f / g.h_eq);
+    P.dx = g.dx;
+    P.dy = g.dy;
+    P.courant = g.courant;
+    P.model_dt = g.model_dt;
+    P.h_eq = g.h_eq;
+    P.gd = g.g;
+    ErrParams& E = c->ep;
+    E.c = g.c_omega;
+    E.nxc = g.nx / g.c_omega;
+    E.nyc = g.ny / g.c_omega;
+    E.dxc = g.c_omega * g.dx;
+    E.dyc = g.c_omega * g.dy;
+    E.inv_c = 1.0 / g.c_omega;
+    E.cx = g.g * g.h_eq / (g.f * 2.0 * g.dx);
+    E.cy = g.g * g.h_eq / (g.f * 2.0 * g.dy);
+    E.cxc = g.g * g.h_eq / (g.f * 2.0 * E.dxc);
+    E.cyc = g.g * g.h_eq / (g.f * 2.0 * E.dyc);
+    for (int db = -2; db <= 2; ++db)
+        for (int da = -2; da <= 2; ++da)
+            E.w[(db + 2) * 5 + (da + 2)] =
+                g.q0 == 0.0 ? 0.0 : soar_kernel(std::hypot(da * E.dxc, db * E.dyc), g.q0, g.l0);
+    E.h_eq = g.h_eq;
+    c->nr = E.nxc * E.nyc;
+}
+
+// Device errors -> the reference's exception message shapes.
+dc_status surface_errors(dc_ctx* ctx) {
+    std::vector<int> err(ctx->M), pos(ctx->M), sub(ctx->M);
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(err.data(), ctx->ctl.err, ctx->M * sizeof(int), cudaMemcpyDeviceToHost));
+    int m = -1;
+    for (int i = 0; i < ctx->M; ++i)
+        if (err[i]) {
+            m = i;
+            break;
+        }
+    if (m < 0) return DC_OK;
+    CU(cudaMemcpy(pos.data(), ctx->ctl.err_pos, ctx->M * sizeof(int), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(sub.data(), ctx->ctl.err_sub, ctx->M * sizeof(int), cudaMemcpyDeviceToHost));
+    const int nx = ctx->cfg.nx;
+    const int p = pos[m];
+    const int j = (p >= 0 && p != 0x7fffffff) ? p % nx : -1;
+    const int k = (p >= 0 && p != 0x7fffffff) ? p / nx : -1;
+    const std::string who = " (particle " + std::to_string(ctx->base + m) + ")";
+    switch (err[m]) {
+    case E_DRY_CELL:
+        if (j >= 0)
+            return set_err(ctx, DC_EDRY,
+                           "flux_rhs: dry cell at (" + std::to_string(j) + "," +
+                               std::to_string(k) + ")" + who,
+                           m, j, k);
+        return set_err(ctx, DC_EDRY, "flux_rhs: dry cell (non-finite eta)" + who, m);
+    case E_DRY_FACE:
+        return set_err(ctx, DC_EDRY, "flux_rhs: dry reconstructed face value" + who, m);
+    case E_NONFINITE:
+        return set_err(ctx, DC_ENONFINITE,
+                       "model_step: non-finite value after substep " + std::to_string(sub[m]) +
+                           who,
+                       m, -1, -1, sub[m]);
+    case E_RUNAWAY:
+        return set_err(ctx, DC_ERUNAWAY, "model_step: substep count exploded" + who, m);
+    case E_DRY_ADD:
+        return set_err(ctx, DC_EDRY, "add_q_half: perturbation dried a cell" + who, m, j, k);
+    case E_DRY_DRIFTER:
+        return set_err(ctx, DC_EDRY, "advect_drifters: dry cell" + who, m);
+    case E_ALPHA:
+        return set_err(ctx, DC_ENONFINITE, "solve_alpha: Lambert-W failure" + who, m);
+    case E_BETA:
+        return set_err(ctx, DC_EINVAL, "sync_target_beta: zeta <= 0 or beta < 0" + who, m);
+    default:
+        return set_err(ctx, DC_ESTATE, "device error " + std::to_string(err[m]) + who, m);
+    }
+}
+
+dc_status check_member(dc_ctx* ctx, int m) {
+    if (m < 0 || m >= ctx->M)
+        return set_err(ctx, DC_ESTATE, "member index " + std::to_string(m) + " out of range");
+    return DC_OK;
+}
+
+// One model step as a graph: cfl_scan -> step_begin -> while(any active){stage1, stage2,
+// substep_end}. The while condition is set on the device by substep_end.
+dc_status build_step_graph(dc_ctx* ctx) {
+    cudaStream_t s = ctx->stream;
+    CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+    launch_step_begin(s, ctx->sp, ctx->ctl);
+    cudaStreamCaptureStatus st;
+    cudaGraph_t cap = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    CU(cudaStreamGetCaptureInfo(s, &st, nullptr, &cap, &deps, &ndeps));
+    cudaGraphConditionalHandle handle;
+    CU(cudaGraphConditionalHandleCreate(&handle, cap, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    CU(cudaGraphAddNode(&cnode, cap, deps, ndeps, &cp));
+    CU(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaStream_t bs;
+    CU(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
+    CU(cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    launch_stage(bs, ctx->sp, ctx->exact, 1, ctx->f[0], ctx->f[1], ctx->f[2], nullptr, nullptr,
+                 nullptr, ctx->f[3], ctx->f[4], ctx->f[5], ctx->ctl);
+    launch_stage(bs, ctx->sp, ctx->exact, 2, ctx->f[3], ctx->f[4], ctx->f[5], ctx->f[0],
+                 ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+    launch_substep_end(bs, ctx->sp, ctx->ctl, static_cast<unsigned long long>(handle), 1);
+    cudaGraph_t body_out = nullptr;
+    CU(cudaStreamEndCapture(bs, &body_out));
+    CU(cudaStreamDestroy(bs));
+    cudaGraph_t g = nullptr;
+    CU(cudaStreamEndCapture(s, &g));
+    CU(cudaGraphInstantiate(&ctx->step_exec, g, 0));
+    CU(cudaGraphDestroy(g));
+    return DC_OK;
+}
+
+// Host-driven fallback (DC_NO_GRAPH=1): guess the substep count from the previous step,
+// then confirm on the host and continue one substep at a time.
+dc_status step_host_loop(dc_ctx* ctx) {
+    cudaStream_t s = ctx->stream;
+    launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+    launch_step_begin(s, ctx->sp, ctx->ctl);
+    ctx->launches += 2;
+    int done = 0;
+    int guess = ctx->last_max_sub;
+    while (true) {
+        for (int i = 0; i < guess; ++i) {
+            launch_stage(s, ctx->sp, ctx->exact, 1, ctx->f[0], ctx->f[1], ctx->f[2], nullptr,
+                         nullptr, nullptr, ctx->f[3], ctx->f[4], ctx->f[5], ctx->ctl);
+            launch_stage(s, ctx->sp, ctx->exact, 2, ctx->f[3], ctx->f[4], ctx->f[5], ctx->f[0],
+                         ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+            launch_substep_end(s, ctx->sp, ctx->ctl, 0ull, 0);
+            ctx->launches += 3;
+        }
+        done += guess;
+        int any = 0;
+        CU(cudaMemcpyAsync(&any, ctx->ctl.any_active, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        if (!any) break;
+        guess = 1;
+    }
+    ctx->last_max_sub = std::max(1, done);
+    return DC_OK;
+}
+
+} // namespace
+
+// small helper kernel: substep iteration counter for launch accounting
+namespace dcg {
+__global__ void count_iters_kernel(const int* sub, int M, unsigned long long* acc) {
+    unsigned long long mx = 0;
+    for (int m = threadIdx.x; m < M; m += blockDim.x) mx = max(mx, (unsigned long long)sub[m]);
+    for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    __shared__ unsigned long long w[32];
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long r = 0;
+        for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) r = max(r, w[i]);
+        *acc += r;
+    }
+}
+} // namespace dcg
+
+extern "C" {
+
+const char* dc_version(void) { return kVersion; }
+
+dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base, int32_t device,
+                    void* stream, dc_ctx** out) {
+    if (!cfg || !out || n_members <= 0) return DC_EINVAL;
+    std::string why;
+    dc_status v = validate(cfg, &why);
+    if (v) {
+        std::fprintf(stderr, "dc_create: %s\n", why.c_str());
+        return v;
+    }
+    dc_ctx* ctx = new dc_ctx();
+    ctx->cfg = *cfg;
+    ctx->M = n_members;
+    ctx->base = member_base;
+    ctx->device = device;
+    ctx->exact = cfg->exact_fp != 0;
+    const char* ng = std::getenv("DC_NO_GRAPH");
+    ctx->use_graph = !(ng && ng[0] == '1');
+    derive_params(ctx);
+    *out = ctx;
+    CU(cudaSetDevice(device));
+    if (stream) {
+        ctx->stream = static_cast<cudaStream_t>(stream);
+    } else {
+        CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    }
+    ctx->field_elems = static_cast<size_t>(ctx->M) * ctx->sp.ny * ctx->sp.pitch;
+    for (int i = 0; i < 6; ++i) {
+        CU(cudaMalloc(&ctx->f[i], ctx->field_elems * sizeof(float)));
+        CU(cudaMemsetAsync(ctx->f[i], 0, ctx->field_elems * sizeof(float), ctx->stream));
+    }
+    const int M = ctx->M;
+    size_t bytes = M * (4 * sizeof(double) + 6 * sizeof(int) + 4 * sizeof(unsigned)) + 64;
+    CU(cudaMalloc(&ctx->ctl_mem, bytes));
+    CU(cudaMemsetAsync(ctx->ctl_mem, 0, bytes, ctx->stream));
+    char* p = static_cast<char*>(ctx->ctl_mem);
+    auto take = [&](size_t n) {
+        char* r = p;
+        p += (n + 15) / 16 * 16;
+        return r;
+    };
+    ctx->ctl.t = reinterpret_cast<double*>(take(M * sizeof(double)));
+    ctx->ctl.t_end = reinterpret_cast<double*>(take(M * sizeof(double)));
+    ctx->ctl.remaining = reinterpret_cast<double*>(take(M * sizeof(double)));
+    ctx->ctl.dt = reinterpret_cast<double*>(take(M * sizeof(double)));
+    ctx->ctl.sub = reinterpret_cast<int*>(take(M * sizeof(int)));
+    ctx->ctl.active = reinterpret_cast<int*>(take(M * sizeof(int)));
+    ctx->ctl.err = reinterpret_cast<int*>(take(M * sizeof(int)));
+    ctx->ctl.err_pos = reinterpret_cast<int*>(take(M * sizeof(int)));
+    ctx->ctl.err_sub = reinterpret_cast<int*>(take(M * sizeof(int)));
+    ctx->ctl.mx = reinterpret_cast<unsigned*>(take(4 * M * sizeof(unsigned)));
+    ctx->ctl.any_active = reinterpret_cast<int*>(take(sizeof(int)));
+    CU(cudaMalloc(&ctx->substep_iters, sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(ctx->substep_iters, 0, sizeof(unsigned long long), ctx->stream));
+    // accumulators: max fields 0, min field all-ones (ordered +inf side), err_pos INT_MAX
+    std::vector<unsigned> mx(4 * M);
+    for (int m = 0; m < M; ++m) {
+        mx[4 * m] = 0u;
+        mx[4 * m + 1] = 0u;
+        mx[4 * m + 2] = 0xffffffffu;
+        mx[4 * m + 3] = 0u;
+    }
+    CU(cudaMemcpyAsync(ctx->ctl.mx, mx.data(), mx.size() * sizeof(unsigned),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<int> big(M, 0x7fffffff);
+    CU(cudaMemcpyAsync(ctx->ctl.err_pos, big.data(), M * sizeof(int), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaMalloc(&ctx->xi, static_cast<size_t>(M) * ctx->nr * sizeof(double)));
+    CU(cudaMalloc(&ctx->corr, static_cast<size_t>(M) * ctx->nr * sizeof(double)));
+    CU(cudaMalloc(&ctx->offs, 2 * M * sizeof(int)));
+    CU(cudaMemsetAsync(ctx->offs, 0, 2 * M * sizeof(int), ctx->stream));
+    CU(cudaMalloc(&ctx->gmax, 2 * M * sizeof(unsigned long long)));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return DC_OK;
+}
+
+dc_status dc_destroy(dc_ctx* ctx) {
+    if (!ctx) return DC_OK;
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->step_exec) cudaGraphExecDestroy(ctx->step_exec);
+    for (auto* q : ctx->f) cudaFree(q);
+    cudaFree(ctx->ctl_mem);
+    cudaFree(ctx->substep_iters);
+    cudaFree(ctx->xi);
+    cudaFree(ctx->corr);
+    cudaFree(ctx->offs);
+    cudaFree(ctx->gmax);
+    cudaFree(ctx->rhs);
+    iewpf_free(ctx->iw);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return DC_OK;
+}
+
+dc_status dc_sync(dc_ctx* ctx) { return surface_errors(ctx); }
+
+const char* dc_last_error(dc_ctx* ctx, int32_t* member, int32_t* j, int32_t* k,
+                          int32_t* substep) {
+    if (!ctx) return "null context";
+    if (member) *member = ctx->em;
+    if (j) *j = ctx->ej;
+    if (k) *k = ctx->ek;
+    if (substep) *substep = ctx->esub;
+    return ctx->err.c_str();
+}
+
+dc_status dc_upload_member(dc_ctx* ctx, int32_t m, const float* eta, const float* hu,
+                           const float* hv, double t) {
+    dc_status st = check_member(ctx, m);
+    if (st) return st;
+    const size_t off = static_cast<size_t>(m) * ctx->sp.ny * ctx->sp.pitch;
+    const float* src[3] = {eta, hu, hv};
+    for (int i = 0; i < 3; ++i)
+        CU(cudaMemcpy2DAsync(ctx->f[i] + off, ctx->sp.pitch * sizeof(float), src[i],
+                             ctx->sp.nx * sizeof(float), ctx->sp.nx * sizeof(float), ctx->sp.ny,
+                             cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->ctl.t + m, &t, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream)); // t is a stack value
+    return DC_OK;
+}
+
+dc_status dc_upload_all(dc_ctx* ctx, const float* eta, const float* hu, const float* hv,
+                        const double* t) {
+    const float* src[3] = {eta, hu, hv};
+    for (int i = 0; i < 3; ++i)
+        CU(cudaMemcpy2DAsync(ctx->f[i], ctx->sp.pitch * sizeof(float), src[i],
+                             ctx->sp.nx * sizeof(float), ctx->sp.nx * sizeof(float),
+                             static_cast<size_t>(ctx->sp.ny) * ctx->M, cudaMemcpyHostToDevice,
+                             ctx->stream));
+    if (t)
+        CU(cudaMemcpyAsync(ctx->ctl.t, t, ctx->M * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+    return DC_OK;
+}
+
+dc_status dc_download_member(dc_ctx* ctx, int32_t m, float* eta, float* hu, float* hv,
+                             double* t) {
+    dc_status st = check_member(ctx, m);
+    if (st) return st;
+    st = surface_errors(ctx);
+    const size_t off = static_cast<size_t>(m) * ctx->sp.ny * ctx->sp.pitch;
+    float* dst[3] = {eta, hu, hv};
+    for (int i = 0; i < 3; ++i)
+        if (dst[i])
+            CU(cudaMemcpy2DAsync(dst[i], ctx->sp.nx * sizeof(float), ctx->f[i] + off,
+                                 ctx->sp.pitch * sizeof(float), ctx->sp.nx * sizeof(float),
+                                 ctx->sp.ny, cudaMemcpyDeviceToHost, ctx->stream));
+    if (t)
+        CU(cudaMemcpyAsync(t, ctx->ctl.t + m, sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return st;
+}
+
+dc_status dc_download_all(dc_ctx* ctx, float* eta, float* hu, float* hv, double* t) {
+    dc_status st = surface_errors(ctx);
+    float* dst[3] = {eta, hu, hv};
+    for (int i = 0; i < 3; ++i)
+        if (dst[i])
+            CU(cudaMemcpy2DAsync(dst[i], ctx->sp.nx * sizeof(float), ctx->f[i],
+                                 ctx->sp.pitch * sizeof(float), ctx->sp.nx * sizeof(float),
+                                 static_cast<size_t>(ctx->sp.ny) * ctx->M, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    if (t)
+        CU(cudaMemcpyAsync(t, ctx->ctl.t, ctx->M * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return st;
+}
+
+// init_double_jet (swe.hpp:459-500): fp64 profile on the host (same libm as the
+// reference build), broadcast to every member, t = 0.
+dc_status dc_init_double_jet(dc_ctx* ctx) {
+    const dc_config& g = ctx->cfg;
+    const int nx = g.nx, ny = g.ny;
+    const double ly = ny * g.dy;
+    const double width = (1.0 / 6.0) * ly, y1 = 0.25 * ly, y2 = 0.75 * ly;
+    const double peak = 0.5 * g.h_eq;
+    auto bump = [&](double y, double yc) {
+        double s = (y - (yc - 0.5 * width)) / width;
+        if (s <= 0.0 || s >= 1.0) return 0.0;
+        return std::exp(4.0) * std::exp(1.0 / ((s - 1.0) * s));
+    };
+    std::vector<double> hu_p(ny), eta_p(ny, 0.0);
+    for (int k = 0; k < ny; ++k) hu_p[k] = peak * (bump((k + 0.5) * g.dy, y1) - bump((k + 0.5) * g.dy, y2));
+    const double cf = g.f / (g.g * g.h_eq);
+    for (int k = 1; k < ny; ++k) eta_p[k] = eta_p[k - 1] - 0.5 * g.dy * cf * (hu_p[k - 1] + hu_p[k]);
+    double mean = 0.0;
+    for (double e : eta_p) mean += e;
+    mean /= ny;
+    for (double& e : eta_p) e -= mean;
+    const int pitch = ctx->sp.pitch;
+    std::vector<float> e(static_cast<size_t>(ny) * pitch, 0.0f), u(e.size(), 0.0f), z(e.size(), 0.0f);
+    for (int k = 0; k < ny; ++k)
+        for (int j = 0; j < nx; ++j) {
+            e[static_cast<size_t>(k) * pitch + j] = static_cast<float>(eta_p[k]);
+            u[static_cast<size_t>(k) * pitch + j] = static_cast<float>(hu_p[k]);
+        }
+    const size_t per = static_cast<size_t>(ny) * pitch;
+    for (int m = 0; m < ctx->M; ++m) {
+        CU(cudaMemcpyAsync(ctx->f[0] + m * per, e.data(), per * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->f[1] + m * per, u.data(), per * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->f[2] + m * per, z.data(), per * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CU(cudaMemsetAsync(ctx->ctl.t, 0, ctx->M * sizeof(double), ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return DC_OK;
+}
+
+dc_status dc_step(dc_ctx* ctx, int32_t n_steps) {
+    if (n_steps < 0) return set_err(ctx, DC_EINVAL, "dc_step: n_steps < 0");
+    if (ctx->use_graph && !ctx->step_exec) {
+        dc_status st = build_step_graph(ctx);
+        if (st) {
+            cudaGetLastError();
+            std::fprintf(stderr, "dc_step: graph path unavailable (%s); using host loop\n",
+                         ctx->err.c_str());
+            ctx->use_graph = false;
+            cudaStreamCaptureStatus cs;
+            if (cudaStreamIsCapturing(ctx->stream, &cs) == cudaSuccess &&
+                cs != cudaStreamCaptureStatusNone) {
+                cudaGraph_t junk;
+                cudaStreamEndCapture(ctx->stream, &junk);
+                if (junk) cudaGraphDestroy(junk);
+            }
+        }
+    }
+    for (int i = 0; i < n_steps; ++i) {
+        if (ctx->use_graph) {
+            CU(cudaGraphLaunch(ctx->step_exec, ctx->stream));
+            dcg::count_iters_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->ctl.sub, ctx->M,
+                                                                ctx->substep_iters);
+            ctx->launches += 3;  // cfl_scan, step_begin, count_iters (+3 per iteration)
+        } else {
+            dc_status st = step_host_loop(ctx);
+            if (st) return st;
+        }
+    }
+    CU(cudaGetLastError());
+    return DC_OK;
+}
+
+dc_status dc_substeps(dc_ctx* ctx, int32_t* out) {
+    CU(cudaMemcpyAsync(out, ctx->ctl.sub, ctx->M * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return DC_OK;
+}
+
+dc_status dc_flux_rhs(dc_ctx* ctx, int32_t m, float* d_eta, float* d_hu, float* d_hv) {
+    dc_status st = check_member(ctx, m);
+    if (st) return st;
+    const size_t per = static_cast<size_t>(ctx->sp.ny) * ctx->sp.pitch;
+    if (!ctx->rhs) CU(cudaMalloc(&ctx->rhs, 3 * per * sizeof(float)));
+    // dry-cell check of load() (swe.hpp:319): flux_rhs throws before computing
+    std::vector<float> e(static_cast<size_t>(ctx->sp.nx) * ctx->sp.ny);
+    CU(cudaMemcpy2DAsync(e.data(), ctx->sp.nx * sizeof(float), ctx->f[0] + m * per,
+                         ctx->sp.pitch * sizeof(float), ctx->sp.nx * sizeof(float), ctx->sp.ny,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    const float H = ctx->sp.H;
+    bool dry = false;
+    for (float v : e) dry |= !(H + v > 0.0f) && !std::isnan(v);
+    if (dry) {
+        for (int k = 0; k < ctx->sp.ny; ++k)
+            for (int j = 0; j < ctx->sp.nx; ++j)
+                if (!(ctx->cfg.h_eq + e[static_cast<size_t>(k) * ctx->sp.nx + j] > 0.0))
+                    return set_err(ctx, DC_EDRY,
+                                   "flux_rhs: dry cell at (" + std::to_string(j) + "," +
+                                       std::to_string(k) + ")",
+                                   m, j, k);
+        return set_err(ctx, DC_EDRY, "flux_rhs: dry cell (non-finite eta)", m);
+    }
+    launch_flux_rhs(ctx->stream, ctx->sp, ctx->exact, m, ctx->f[0], ctx->f[1], ctx->f[2],
+                    ctx->rhs, ctx->rhs + per, ctx->rhs + 2 * per, ctx->ctl);
+    ctx->launches += 1;
+    float* dst[3] = {d_eta, d_hu, d_hv};
+    for (int i = 0; i < 3; ++i)
+        CU(cudaMemcpy2DAsync(dst[i], ctx->sp.nx * sizeof(float), ctx->rhs + i * per,
+                             ctx->sp.pitch * sizeof(float), ctx->sp.nx * sizeof(float),
+                             ctx->sp.ny, cudaMemcpyDeviceToHost, ctx->stream));
+    return surface_errors(ctx);
+}
+
+dc_status dc_cfl_dt(dc_ctx* ctx, double* dt_out) {
+    const int M = ctx->M;
+    CU(cudaMemsetAsync(ctx->gmax, 0, 2 * M * sizeof(unsigned long long), ctx->stream));
+    std::vector<int> big(M, 0x7fffffff);
+    CU(cudaMemcpyAsync(ctx->ctl.err_pos, big.data(), M * sizeof(int), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    launch_cfl_public(ctx->stream, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->gmax,
+                      ctx->ctl.err_pos);
+    ctx->launches += 1;
+    std::vector<unsigned long long> g(2 * M);
+    std::vector<int> pos(M);
+    CU(cudaMemcpyAsync(g.data(), ctx->gmax, g.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(pos.data(), ctx->ctl.err_pos, M * sizeof(int), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int m = 0; m < M; ++m) {
+        if (pos[m] != 0x7fffffff) {
+            const int j = pos[m] % ctx->sp.nx, k = pos[m] / ctx->sp.nx;
+            CU(cudaMemcpyAsync(ctx->ctl.err_pos, big.data(), M * sizeof(int),
+                               cudaMemcpyHostToDevice, ctx->stream));
+            CU(cudaStreamSynchronize(ctx->stream));
+            return set_err(ctx, DC_EDRY,
+                           "cfl_dt: dry cell at (" + std::to_string(j) + "," + std::to_string(k) + ")",
+                           m, j, k);
+        }
+        double gx, gy;
+        std::memcpy(&gx, &g[2 * m], 8);
+        std::memcpy(&gy, &g[2 * m + 1], 8);
+        dt_out[m] = ctx->cfg.courant * 0.25 * std::min(ctx->cfg.dx / gx, ctx->cfg.dy / gy);
+    }
+    return DC_OK;
+}
+
+dc_status dc_perturb(dc_ctx* ctx, int32_t mode, const int32_t* offsets, const double* xi) {
+    if (ctx->cfg.q0 == 0.0) return DC_OK; // stochastic.hpp:167: consumes no randomness
+    const int M = ctx->M;
+    if (mode == DC_NOISE_PHILOX) {
+        launch_philox_noise(ctx->stream, ctx->ep, M, ctx->cfg.seed, 1 /*model_error*/, ctx->base, 0,
+                            ctx->me_draw, ctx->xi, ctx->offs, ctx->ctl.err);
+        ctx->me_draw += 1;
+    } else if (mode == DC_NOISE_INJECTED) {
+        if (!offsets || !xi) return set_err(ctx, DC_EINVAL, "dc_perturb: injected noise missing");
+        for (int m = 0; m < 2 * M; ++m)
+            if (offsets[m] < 0 || offsets[m] >= ctx->cfg.c_omega)
+                return set_err(ctx, DC_EINVAL, "CoarseGrid: offsets must lie in [0, c_omega)");
+        CU(cudaMemcpyAsync(ctx->offs, offsets, 2 * M * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->xi, xi, static_cast<size_t>(M) * ctx->nr * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream)); // host buffers may be reused on return
+    } else {
+        return set_err(ctx, DC_EINVAL, "dc_perturb: unknown noise mode");
+    }
+    launch_coarse_soar(ctx->stream, ctx->ep, M, ctx->xi, ctx->corr, ctx->ctl.err);
+    launch_q_half_apply(ctx->stream, ctx->sp, ctx->ep, ctx->corr, ctx->offs, 1.0, ctx->f[0],
+                        ctx->f[1], ctx->f[2], ctx->ctl.err, ctx->ctl.err_pos, M);
+    ctx->launches += (mode == DC_NOISE_PHILOX) ? 3 : 2;
+    CU(cudaGetLastError());
+    return DC_OK;
+}
+
+dc_status dc_add_q_half(dc_ctx* ctx, const int32_t* offsets, const double* coarse, double scale) {
+    const int M = ctx->M;
+    for (int m = 0; m < 2 * M; ++m)
+        if (offsets[m] < 0 || offsets[m] >= ctx->cfg.c_omega)
+            return set_err(ctx, DC_EINVAL, "CoarseGrid: offsets must lie in [0, c_omega)");
+    CU(cudaMemcpyAsync(ctx->offs, offsets, 2 * M * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->xi, coarse, static_cast<size_t>(M) * ctx->nr * sizeof(double),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    launch_coarse_soar(ctx->stream, ctx->ep, M, ctx->xi, ctx->corr, ctx->ctl.err);
+    launch_q_half_apply(ctx->stream, ctx->sp, ctx->ep, ctx->corr, ctx->offs, scale, ctx->f[0],
+                        ctx->f[1], ctx->f[2], ctx->ctl.err, ctx->ctl.err_pos, M);
+    ctx->launches += 2;
+    CU(cudaGetLastError());
+    return DC_OK;
+}
+
+dc_status dc_get_draw_counter(dc_ctx* ctx, uint64_t* d) {
+    *d = ctx->me_draw;
+    return DC_OK;
+}
+
+dc_status dc_set_draw_counter(dc_ctx* ctx, uint64_t d) {
+    ctx->me_draw = d;
+    return DC_OK;
+}
+
+int64_t dc_kernel_launches(dc_ctx* ctx) {
+    // graph path: 2 kernels per step + 3 per substep iteration (counted on the device)
+    unsigned long long iters = 0;
+    if (ctx->use_graph && ctx->substep_iters) {
+        cudaMemcpyAsync(&iters, ctx->substep_iters, sizeof(iters), cudaMemcpyDeviceToHost,
+                        ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+    }
+    return ctx->launches + 3 * static_cast<int64_t>(iters);
+}
+
+void* dc_stream(dc_ctx* ctx) { return ctx->stream; }
+
+} // extern "C"
+
+// IEWPF / observation entry points live in iewpf_api.cu; they need the context layout.
+#include "iewpf_api.inc"

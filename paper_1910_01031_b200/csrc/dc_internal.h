@@ -1,0 +1,86 @@
+// dc_internal.h -- private structures shared by the CUDA translation units and the
+// C-ABI implementation (api.cu). Not part of the public boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/driftcast_gpu.h"
+
+namespace dcg {
+
+// device-side error codes (first error per member wins, atomicCAS from 0)
+enum DevErr : int {
+    E_NONE = 0,
+    E_DRY_CELL = 2,      // "flux_rhs: dry cell at (j,k)"           (swe.hpp:324-331)
+    E_NONFINITE = 3,     // "model_step: non-finite value after substep k" (swe.hpp:416-418)
+    E_RUNAWAY = 4,       // "model_step: substep count exploded"   (swe.hpp:255-256)
+    E_DRY_FACE = 12,     // "flux_rhs: dry reconstructed face value" (swe.hpp:374-375)
+    E_DRY_ADD = 22,      // "add_q_half: perturbation dried a cell" (stochastic.hpp:159)
+    E_DRY_DRIFTER = 32,  // "advect_drifters: dry cell at (j,k)"
+    E_ALPHA = 42,        // "solve_alpha: ..."
+    E_BETA = 52,         // "sync_target_beta: ..."
+};
+
+// Constants of the shallow-water stencil, derived exactly as the reference's Stepper
+// derives them (double, then one rounding to float): swe.hpp:277-278,340-344,356-357,380-382.
+struct SweParams {
+    int nx, ny, pitch, M;
+    int by, strips;       // rows per CTA strip, strips per member
+    float H, g, theta, cf_x, cf_y, inv_g, idx, idy, fH;
+    double dx, dy, courant, model_dt, h_eq, gd;
+};
+
+// Per-member control block for the device-side CFL substep loop (swe.hpp:244-259).
+struct StepCtl {
+    double* t;          // simulation time
+    double* t_end;      // t + model_dt of the step in progress
+    double* remaining;  // seconds left in the step
+    double* dt;         // dt of the substep about to run
+    int* sub;           // substep index within the step
+    int* active;        // 1 while remaining > 0
+    int* err;           // DevErr
+    int* err_pos;       // k*nx+j of the first dry cell found (atomicMin)
+    int* err_sub;       // substep index of a non-finite failure
+    unsigned* mx;       // [M][4]: max|u|+c bits, max|v|+c bits, ordered min h, spare
+    int* any_active;    // loop condition (host-visible in the fallback path)
+};
+
+struct ErrParams {
+    int c, nxc, nyc;
+    double dxc, dyc;
+    double inv_c;         // 1.0 / c_omega (stochastic.hpp:96)
+    double cx, cy;        // g*H/(f*2*dx), g*H/(f*2*dy)  (stochastic.hpp:127-128)
+    double cxc, cyc;      // same at coarse spacing (stochastic.hpp:181-182)
+    double w[25];         // SOAR weights w[(db+2)*5 + (da+2)] (stochastic.hpp:54-57)
+    double h_eq;
+};
+
+// stochastic.cu launchers
+void launch_philox_noise(cudaStream_t s, const ErrParams& ep, int M, uint64_t seed, uint64_t tag,
+                         int64_t member_base, uint32_t substream, uint64_t draw, double* xi,
+                         int* offsets, const int* err);
+void launch_coarse_soar(cudaStream_t s, const ErrParams& ep, int M, const double* in,
+                        double* out, const int* err);
+void launch_q_half_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
+                         const double* corr, const int* offsets, double scale, float* eta,
+                         float* hu, float* hv, int* err, int* err_pos, int M);
+
+// swe.cu launchers
+void launch_cfl_scan(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
+                     const float* hv, StepCtl ctl);
+void launch_step_begin(cudaStream_t s, const SweParams& sp, StepCtl ctl);
+void launch_stage(cudaStream_t s, const SweParams& sp, bool exact, int stage, const float* ie,
+                  const float* iu, const float* iv, const float* s0e, const float* s0u,
+                  const float* s0v, float* oe, float* ou, float* ov, StepCtl ctl);
+void launch_substep_end(cudaStream_t s, const SweParams& sp, StepCtl ctl,
+                        unsigned long long cond_handle, int use_cond);
+void launch_cfl_public(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
+                       const float* hv, unsigned long long* gmax, int* dry_pos);
+void launch_flux_rhs(cudaStream_t s, const SweParams& sp, bool exact, int m, const float* eta,
+                     const float* hu, const float* hv, float* re, float* ru, float* rv,
+                     StepCtl ctl);
+
+} // namespace dcg

@@ -1,0 +1,41 @@
+// iewpf_host.h -- device buffers of the observation / drifter / IEWPF stages.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace dcg {
+
+struct IewpfBuffers {
+    int cap_obs = 0;          // capacity (observations)
+    int n_obs = 0;
+    double* obs = nullptr;    // [n_obs][4] x, y, y_hu, y_hv
+    int* cells = nullptr;     // [n_obs][2] containing cell (j,k)
+    double* d = nullptr;      // [M][n_obs][2] innovations
+    double* sd = nullptr;     // [M][n_obs][2] S*d
+    double* win = nullptr;    // [M][n_obs][121] pull windows (SOAR(SOAR(dipole)))
+    int* tile_lists = nullptr;// [n_tiles][cap_obs] obs ids per fine tile (ascending)
+    int* tile_count = nullptr;// [n_tiles]
+    double* nu = nullptr;     // [M][nr]
+    double* scal = nullptr;   // [M][8]: c, phi, gamma, zeta, alpha, xx, nn, nx
+    double* cz = nullptr;     // [M][2] local (c, zeta)
+    double* cz_all = nullptr; // [cap_total][2]
+    int cap_total = 0;
+    double* wb = nullptr;     // [2] w_target, beta
+    double* S = nullptr;      // [4]
+    double* usig = nullptr;   // [49*49]
+    int* foffs = nullptr;     // [M][2] filter-grid offsets
+    // drifters
+    int n_d = 0;
+    double* dpos = nullptr;   // [M][n_d][2]
+    int* dwind = nullptr;     // [M][n_d][2]
+};
+
+inline void iewpf_free(IewpfBuffers& b) {
+    void* ps[] = {b.obs, b.cells, b.d, b.sd, b.win, b.tile_lists, b.tile_count, b.nu, b.scal,
+                  b.cz, b.cz_all, b.wb, b.S, b.usig, b.foffs, b.dpos, b.dwind};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    b = IewpfBuffers{};
+}
+
+} // namespace dcg

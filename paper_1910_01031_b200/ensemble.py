@@ -1,0 +1,288 @@
+"""Python handle on one GPU ensemble context (the C ABI of include/driftcast_gpu.h).
+
+Method names follow the reference operator surface they replace
+(/root/reference/proj/include/driftcast/*.hpp and SPEC.md): ``model_step`` is
+Stepper::model_step over every member, ``perturb_state`` is perturb_state, etc.
+Host arrays use the reference layout (row-major, j fastest; member-major).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import DcConfig, DcError, DcObs, DcParticleDiag
+
+
+@dataclass
+class Config:
+    """ModelGrid + PhysParams + SchemeParams + ErrorParams (+ seed): paper defaults
+    (§5): 500x300 double jet, dx=dy=2220 m, c_Omega=5,
+    L0 = 3/4 coarse spacing, q0 = 2.5e-4."""
+
+    nx: int = 500
+    ny: int = 300
+    dx: float = 2220.0
+    dy: float = 2220.0
+    g: float = 9.806
+    f: float = 1.405e-4
+    h_eq: float = 230.0
+    courant: float = 0.8
+    limiter_theta: float = 1.3
+    model_dt: float = 60.0
+    q0: float = 2.5e-4
+    l0: float | None = None
+    c_omega: int = 5
+    seed: int = 1
+    exact_fp: bool = True
+
+    def to_c(self) -> DcConfig:
+        l0 = self.l0 if self.l0 is not None else 0.75 * self.c_omega * self.dx
+        return DcConfig(self.nx, self.ny, self.dx, self.dy, self.g, self.f, self.h_eq,
+                        self.courant, self.limiter_theta, self.model_dt, self.q0, l0,
+                        self.c_omega, 2, self.seed, 1 if self.exact_fp else 0, 0)
+
+    @property
+    def nr(self) -> int:
+        return (self.nx // self.c_omega) * (self.ny // self.c_omega)
+
+
+def _f(a):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _d(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _i(a):
+    return a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def obs_array(obs) -> C.Array:
+    """(n,4) array of (x, y, y_hu, y_hv) -> dc_obs[n]."""
+    obs = np.ascontiguousarray(obs, np.float64).reshape(-1, 4)
+    arr = (DcObs * max(1, obs.shape[0]))()
+    C.memmove(arr, obs.ctypes.data, obs.nbytes)
+    return arr
+
+
+class Ensemble:
+    """N_e particles of the double-jet shallow-water model resident on one GPU."""
+
+    def __init__(self, cfg: Config, n_members: int, member_base: int = 0, device: int = 0,
+                 stream: int | None = None):
+        self.L = _lib.load()
+        self.cfg = cfg
+        self.n = n_members
+        self.base = member_base
+        self._c = cfg.to_c()
+        h = C.c_void_p()
+        rc = self.L.dc_create(C.byref(self._c), n_members, member_base, device,
+                              C.c_void_p(stream) if stream else None, C.byref(h))
+        if rc:
+            raise DcError(rc, "dc_create failed (see stderr)")
+        self.h = h
+
+    # ---- plumbing ----
+    def _ck(self, rc):
+        if rc:
+            m, j, k, s = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+            msg = self.L.dc_last_error(self.h, C.byref(m), C.byref(j), C.byref(k), C.byref(s))
+            raise DcError(rc, msg.decode(), m.value, j.value, k.value, s.value)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.dc_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        self._ck(self.L.dc_sync(self.h))
+
+    @property
+    def stream(self) -> int:
+        return self.L.dc_stream(self.h) or 0
+
+    def kernel_launches(self) -> int:
+        return int(self.L.dc_kernel_launches(self.h))
+
+    # ---- state I/O ----
+    def upload(self, eta, hu, hv, t=None):
+        eta, hu, hv = (np.ascontiguousarray(a, np.float32) for a in (eta, hu, hv))
+        tt = None if t is None else np.ascontiguousarray(np.broadcast_to(t, (self.n,)), np.float64)
+        self._ck(self.L.dc_upload_all(self.h, _f(eta), _f(hu), _f(hv),
+                                      _d(tt) if tt is not None else None))
+        self.sync()
+
+    def upload_member(self, m, eta, hu, hv, t=0.0):
+        eta, hu, hv = (np.ascontiguousarray(a, np.float32) for a in (eta, hu, hv))
+        self._ck(self.L.dc_upload_member(self.h, m, _f(eta), _f(hu), _f(hv), t))
+
+    def download(self):
+        shp = (self.n, self.cfg.ny, self.cfg.nx)
+        e, u, v = (np.empty(shp, np.float32) for _ in range(3))
+        t = np.empty(self.n, np.float64)
+        self._ck(self.L.dc_download_all(self.h, _f(e), _f(u), _f(v), _d(t)))
+        return e, u, v, t
+
+    def download_member(self, m):
+        shp = (self.cfg.ny, self.cfg.nx)
+        e, u, v = (np.empty(shp, np.float32) for _ in range(3))
+        t = C.c_double()
+        self._ck(self.L.dc_download_member(self.h, m, _f(e), _f(u), _f(v), C.byref(t)))
+        return e, u, v, t.value
+
+    # ---- model operator ----
+    def init_double_jet(self):
+        self._ck(self.L.dc_init_double_jet(self.h))
+
+    def model_step(self, n_steps: int = 1):
+        self._ck(self.L.dc_step(self.h, n_steps))
+
+    def flux_rhs(self, m=0):
+        shp = (self.cfg.ny, self.cfg.nx)
+        out = [np.empty(shp, np.float32) for _ in range(3)]
+        self._ck(self.L.dc_flux_rhs(self.h, m, *[_f(o) for o in out]))
+        return out
+
+    def cfl_dt(self):
+        out = np.empty(self.n, np.float64)
+        self._ck(self.L.dc_cfl_dt(self.h, _d(out)))
+        return out
+
+    def substeps(self):
+        out = np.empty(self.n, np.int32)
+        self._ck(self.L.dc_substeps(self.h, _i(out)))
+        return out
+
+    # ---- model error ----
+    def perturb_state(self, offsets=None, xi=None):
+        """perturb_state on every member: Philox draw, or injected (offsets, xi)."""
+        if offsets is None:
+            self._ck(self.L.dc_perturb(self.h, _lib.DC_NOISE_PHILOX, None, None))
+        else:
+            offsets = np.ascontiguousarray(offsets, np.int32).reshape(self.n, 2)
+            xi = np.ascontiguousarray(xi, np.float64).reshape(self.n, self.cfg.nr)
+            self._ck(self.L.dc_perturb(self.h, _lib.DC_NOISE_INJECTED, _i(offsets), _d(xi)))
+
+    def add_q_half(self, offsets, coarse, scale=1.0):
+        offsets = np.ascontiguousarray(offsets, np.int32).reshape(self.n, 2)
+        coarse = np.ascontiguousarray(coarse, np.float64).reshape(self.n, self.cfg.nr)
+        self._ck(self.L.dc_add_q_half(self.h, _i(offsets), _d(coarse), scale))
+
+    @property
+    def draw_counter(self) -> int:
+        v = C.c_uint64()
+        self._ck(self.L.dc_get_draw_counter(self.h, C.byref(v)))
+        return v.value
+
+    @draw_counter.setter
+    def draw_counter(self, v: int):
+        self._ck(self.L.dc_set_draw_counter(self.h, v))
+
+    # ---- observation system ----
+    def innovations(self, obs):
+        arr = obs_array(obs)
+        n = len(np.asarray(obs).reshape(-1, 4))
+        out = np.empty((self.n, n, 2), np.float64)
+        self._ck(self.L.dc_innovations(self.h, arr, n, _d(out)))
+        return out
+
+    def observe_mooring(self, m, xy):
+        xy = np.ascontiguousarray(xy, np.float64).reshape(-1, 2)
+        out = np.empty((xy.shape[0], 2), np.float64)
+        self._ck(self.L.dc_observe_mooring(self.h, m, _d(xy), xy.shape[0], _d(out)))
+        return out
+
+    def drifters_set(self, pos):
+        pos = np.ascontiguousarray(pos, np.float64)
+        if pos.ndim == 2:
+            pos = np.ascontiguousarray(np.broadcast_to(pos, (self.n,) + pos.shape))
+        self.n_drifters = pos.shape[1]
+        self._ck(self.L.dc_drifters_set(self.h, _d(pos), pos.shape[1]))
+
+    def advect_drifters(self, dt):
+        self._ck(self.L.dc_drifters_advect(self.h, dt))
+
+    def drifters_get(self):
+        pos = np.empty((self.n, self.n_drifters, 2), np.float64)
+        wind = np.empty((self.n, self.n_drifters, 2), np.int32)
+        self._ck(self.L.dc_drifters_get(self.h, _d(pos), _i(wind)))
+        return pos, wind
+
+    # ---- IEWPF ----
+    def iewpf_assimilate(self, obs, S, usig, cycle):
+        arr = obs_array(obs)
+        n = len(np.asarray(obs).reshape(-1, 4))
+        S = np.ascontiguousarray(S, np.float64).reshape(4)
+        usig = np.ascontiguousarray(usig, np.float64).reshape(49 * 49)
+        self._ck(self.L.dc_iewpf_assimilate(self.h, arr, n, _d(S), _d(usig), cycle))
+
+    def iewpf_begin(self, obs, S, usig, cycle, n_total, cz_out=None, cz_ptr=None):
+        """Stages 1-3; writes this slice's (c, zeta) to a host array or a device pointer."""
+        arr = obs_array(obs)
+        n = len(np.asarray(obs).reshape(-1, 4))
+        S = np.ascontiguousarray(S, np.float64).reshape(4)
+        usig = np.ascontiguousarray(usig, np.float64).reshape(49 * 49)
+        if cz_ptr is not None:
+            self._ck(self.L.dc_iewpf_begin(self.h, arr, n, _d(S), _d(usig), cycle, n_total,
+                                           C.c_void_p(cz_ptr), 1))
+            return None
+        out = np.empty((self.n, 2), np.float64) if cz_out is None else cz_out
+        self._ck(self.L.dc_iewpf_begin(self.h, arr, n, _d(S), _d(usig), cycle, n_total,
+                                       out.ctypes.data_as(C.c_void_p), 0))
+        return out
+
+    def iewpf_finish(self, cz_all=None, cz_ptr=None):
+        if cz_ptr is not None:
+            self._ck(self.L.dc_iewpf_finish(self.h, C.c_void_p(cz_ptr), 1))
+        else:
+            cz = np.ascontiguousarray(cz_all, np.float64)
+            self._ck(self.L.dc_iewpf_finish(self.h, cz.ctypes.data_as(C.c_void_p), 0))
+
+    def iewpf_diagnostics(self):
+        d = (DcParticleDiag * self.n)()
+        wb = np.empty(2, np.float64)
+        self._ck(self.L.dc_iewpf_diagnostics(self.h, d, _d(wb)))
+        arr = np.array([[x.c, x.phi, x.gamma, x.zeta, x.alpha] for x in d], np.float64)
+        return arr, wb
+
+    def da_cycle(self, n_steps, obs, S, usig, cycle):
+        arr = obs_array(obs)
+        n = len(np.asarray(obs).reshape(-1, 4))
+        S = np.ascontiguousarray(S, np.float64).reshape(4)
+        usig = np.ascontiguousarray(usig, np.float64).reshape(49 * 49)
+        self._ck(self.L.dc_da_cycle(self.h, n_steps, arr, n, _d(S), _d(usig), cycle))
+
+
+def precompute_S(cfg: Config, r_hu=1.0, r_hv=1.0):
+    """precompute_S: returns (HQH^T, S) as 2x2 arrays."""
+    L = _lib.load()
+    c = cfg.to_c()
+    h = np.empty(4, np.float64)
+    s = np.empty(4, np.float64)
+    rc = L.dc_precompute_S(C.byref(c), r_hu, r_hv, _d(h), _d(s))
+    if rc:
+        raise DcError(rc, "dc_precompute_S failed")
+    return h.reshape(2, 2), s.reshape(2, 2)
+
+
+def precompute_local_svd(cfg: Config, S):
+    """precompute_local_svd: returns (block, U Sigma^{1/2}) 49x49."""
+    L = _lib.load()
+    c = cfg.to_c()
+    S = np.ascontiguousarray(S, np.float64).reshape(4)
+    b = np.empty((49, 49), np.float64)
+    u = np.empty((49, 49), np.float64)
+    rc = L.dc_precompute_local_svd(C.byref(c), _d(S), _d(b), _d(u))
+    if rc:
+        raise DcError(rc, "dc_precompute_local_svd failed")
+    return b, u

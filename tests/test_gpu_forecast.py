@@ -1,0 +1,237 @@
+"""GPU parity of the forecast path (model operator M + model error) through the C ABI.
+
+The CUDA path is compared with the CPU restatement (oracle/liboracle.so) on the same
+inputs. In the exact build (dc_config.exact_fp = 1) every float/double op follows the
+reference's evaluation order without contraction, so the bar is BITWISE equality
+(np.array_equal on float values: +0 == -0). The FMA build is held to the tolerance the
+survey derived from the reference itself under FMA:
+max|diff| <= 1e-5 * max|field| over a <= 1-day horizon.
+Known answers re-hosted from proj/tests/test_swe.cpp and test_stochastic.cpp.
+"""
+import numpy as np
+import pytest
+
+from checkers import State, make_params
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1910_01031_b200 import Config, Ensemble
+    return Config, Ensemble
+
+
+def cfg_pair(nx=500, ny=300, exact=True, **kw):
+    Config, _ = _gpu()
+    cfg = Config(nx=nx, ny=ny, exact_fp=exact, **kw)
+    p = make_params(nx=nx, ny=ny, q0=cfg.q0, seed=cfg.seed, c_omega=cfg.c_omega,
+                    dx=cfg.dx, dy=cfg.dy)
+    return cfg, p
+
+
+def perturbed_jets(oracle, p, n, seed=0, amp_eta=0.02, amp_v=2.0):
+    """Double jet plus smooth member-specific perturbations (deterministic)."""
+    base = oracle.init_double_jet(p)
+    rng = np.random.default_rng(seed)
+    y, x = np.mgrid[0:p.ny, 0:p.nx]
+    eta = np.empty((n, p.ny, p.nx), np.float32)
+    hu, hv = np.empty_like(eta), np.empty_like(eta)
+    for m in range(n):
+        kx, ky = rng.integers(1, 4, size=2)
+        ph = rng.uniform(0, 2 * np.pi, size=3)
+        bump = np.sin(2 * np.pi * kx * x / p.nx + ph[0]) * np.cos(2 * np.pi * ky * y / p.ny + ph[1])
+        eta[m] = base.eta + (amp_eta * bump).astype(np.float32)
+        hu[m] = base.hu + (amp_v * np.cos(2 * np.pi * ky * y / p.ny + ph[2])).astype(np.float32)
+        hv[m] = (amp_v * bump).astype(np.float32)
+    return eta, hu, hv
+
+
+def test_flux_rhs_bitwise(oracle):
+    _, Ensemble = _gpu()
+    for nx, ny in [(500, 300), (100, 60), (16, 12)]:
+        cfg, p = cfg_pair(nx, ny)
+        e, u, v = perturbed_jets(oracle, p, 2, seed=nx)
+        ens = Ensemble(cfg, 2)
+        ens.upload(e, u, v, 0.0)
+        for m in range(2):
+            g = ens.flux_rhs(m)
+            o = oracle.flux_rhs(p, State(e[m].copy(), u[m].copy(), v[m].copy()))
+            for a, b in zip(g, o):
+                assert np.array_equal(a, b), (nx, ny, m, np.abs(a - b).max())
+        ens.close()
+
+
+def test_lake_at_rest_exact_zero():
+    """test_swe.cpp:17-44: zero tendencies, bitwise-preserved rest state, t advanced."""
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair(16, 12)
+    ens = Ensemble(cfg, 2)
+    z = np.zeros((2, 12, 16), np.float32)
+    lifted = z.copy()
+    lifted[1] = 0.1
+    ens.upload(lifted, z, z, 0.0)
+    for m in range(2):
+        for r in ens.flux_rhs(m):
+            assert np.abs(r).max() == 0.0
+    ens.model_step(1)
+    e, u, v, t = ens.download()
+    assert np.array_equal(e, lifted) and np.all(u == 0) and np.all(v == 0)
+    assert np.all(t == 60.0)
+
+
+def test_model_step_bitwise_10_members(oracle):
+    """Config 1 (500x300, 10 members): 3 model steps bitwise equal to the oracle,
+    including the per-member substep sequences."""
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair()
+    n = 10
+    e, u, v = perturbed_jets(oracle, p, n, seed=3)
+    ens = Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    ens.model_step(3)
+    ge, gu, gv, gt = ens.download()
+    subs = ens.substeps()
+    for m in range(n):
+        s = State(e[m].copy(), u[m].copy(), v[m].copy(), 0.0)
+        dts = oracle.model_step(p, s, 3)
+        assert np.array_equal(ge[m], s.eta), (m, np.abs(ge[m] - s.eta).max())
+        assert np.array_equal(gu[m], s.hu)
+        assert np.array_equal(gv[m], s.hv)
+        assert gt[m] == s.t == 180.0
+        assert subs[m] == len(dts)
+    ens.close()
+
+
+def test_model_step_fma_tolerance(oracle):
+    """FMA build: within 1e-5 of max|field| after 10 steps."""
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair(exact=False)
+    n = 4
+    e, u, v = perturbed_jets(oracle, p, n, seed=5)
+    ens = Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    ens.model_step(10)
+    ge, gu, gv, _ = ens.download()
+    for m in range(n):
+        s = State(e[m].copy(), u[m].copy(), v[m].copy(), 0.0)
+        oracle.model_step(p, s, 10)
+        for a, b in ((ge[m], s.eta), (gu[m], s.hu), (gv[m], s.hv)):
+            assert np.abs(a - b).max() <= 1e-5 * max(np.abs(b).max(), 1e-30)
+    ens.close()
+
+
+def test_cfl_dt_public_formula(oracle):
+    """Stepper::cfl_dt (swe.hpp:212-226) and test_swe.cpp:46-62."""
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair(16, 16)
+    ens = Ensemble(cfg, 2)
+    z = np.zeros((2, 16, 16), np.float32)
+    hu = z.copy()
+    hu[1] = 230.0
+    ens.upload(z, hu, z, 0.0)
+    dt = ens.cfl_dt()
+    expect = 0.8 * 0.25 * 2220.0 / np.sqrt(9.806 * 230.0)
+    assert abs(dt[0] - expect) <= 1e-3 * expect
+    assert dt[1] < dt[0]
+    assert dt[0] == oracle.cfl_dt(p, State(z[0], z[0], z[0]))
+
+
+def test_perturb_injected_bitwise(oracle, ref):
+    """perturb_state with the reference's own NoiseStream draws injected: the GPU
+    reproduces the reference perturb_state bit-for-bit."""
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair()
+    n = 3
+    e, u, v = perturbed_jets(oracle, p, n, seed=9)
+    ens = Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    offs, xis, refs = [], [], []
+    for m in range(n):
+        s = State(e[m].copy(), u[m].copy(), v[m].copy())
+        o, xi = ref.perturb(p, s, 1, 1, m, 1)
+        offs.append(o[0])
+        xis.append(xi[0])
+        refs.append(s)
+    ens.perturb_state(np.array(offs), np.array(xis))
+    ge, gu, gv, _ = ens.download()
+    for m in range(n):
+        assert np.array_equal(ge[m], refs[m].eta)
+        assert np.array_equal(gu[m], refs[m].hu)
+        assert np.array_equal(gv[m], refs[m].hv)
+
+
+def test_perturb_philox_bitwise(oracle):
+    """Counter-based Philox model error: GPU == CPU restatement, several draws."""
+    _, Ensemble = _gpu()
+    for nx, ny, c in [(500, 300, 5), (60, 60, 5), (30, 27, 3)]:
+        cfg, p = cfg_pair(nx, ny, c_omega=c)
+        n = 3
+        e, u, v = perturbed_jets(oracle, p, n, seed=11)
+        ens = Ensemble(cfg, n, member_base=7)
+        ens.upload(e, u, v, 0.0)
+        for _ in range(2):
+            ens.perturb_state()
+        ge, gu, gv, _ = ens.download()
+        for m in range(n):
+            s = State(e[m].copy(), u[m].copy(), v[m].copy())
+            for d in range(2):
+                oracle.perturb_philox(p, s, 7 + m, d)
+            assert np.array_equal(ge[m], s.eta), (nx, m)
+            assert np.array_equal(gu[m], s.hu)
+            assert np.array_equal(gv[m], s.hv)
+        ens.close()
+
+
+def test_step_perturb_sequence_bitwise(oracle):
+    """Forecast with model error, 5 model steps with a Philox draw after each of the
+    first 4 (the DA-cycle forecast pattern), bitwise."""
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair()
+    n = 4
+    e, u, v = perturbed_jets(oracle, p, n, seed=21)
+    ens = Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    for s in range(5):
+        ens.model_step(1)
+        if s < 4:
+            ens.perturb_state()
+    ge, gu, gv, gt = ens.download()
+    for m in range(n):
+        st = State(e[m].copy(), u[m].copy(), v[m].copy(), 0.0)
+        for s in range(5):
+            oracle.model_step(p, st, 1)
+            if s < 4:
+                oracle.perturb_philox(p, st, m, s)
+        assert np.array_equal(ge[m], st.eta) and np.array_equal(gu[m], st.hu)
+        assert np.array_equal(gv[m], st.hv) and gt[m] == st.t
+
+
+def test_dry_cell_rejected():
+    """test_swe.cpp:235-243: DryCellError on a dry cell."""
+    _, Ensemble = _gpu()
+    from paper_1910_01031_b200 import DcError
+    cfg, p = cfg_pair(16, 12)
+    ens = Ensemble(cfg, 1)
+    z = np.zeros((1, 12, 16), np.float32)
+    e = z.copy()
+    e[0, 4, 3] = -231.0
+    ens.upload(e, z, z, 0.0)
+    with pytest.raises(DcError) as ei:
+        ens.flux_rhs(0)
+    assert ei.value.status == 2 and "dry cell at (3,4)" in ei.value.message
+    with pytest.raises(DcError) as ei:
+        ens.cfl_dt()
+    assert ei.value.status == 2
+
+
+def test_double_jet_init_matches(oracle):
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair()
+    ens = Ensemble(cfg, 2)
+    ens.init_double_jet()
+    e, u, v, t = ens.download()
+    s = oracle.init_double_jet(p)
+    assert np.array_equal(e[1], s.eta) and np.array_equal(u[1], s.hu) and np.all(v == 0)
