@@ -167,8 +167,12 @@ dc_status dc_da_cycle(dc_ctx* ctx, int32_t n_steps, const dc_obs* obs, int32_t n
 /* ---- instrumentation ------------------------------------------------------------ */
 /* number of kernels this context has launched (host-side counter). */
 int64_t dc_kernel_launches(dc_ctx* ctx);
-/* device pointers (for external collectives / profiling); may be NULL. */
+/* the cudaStream_t the context runs on. */
 void* dc_stream(dc_ctx* ctx);
+/* Exhaustive device self-check of the branch-free IEEE sqrt / reciprocal used by the
+ * stencil against the CUDA intrinsics over all positive normal floats (synchronous).
+ * counts[0..1] = sqrt / rcp mismatches, counts[2..3] = first mismatching operand bits. */
+dc_status dc_selftest_math(int32_t device, uint64_t* counts);
 
 #ifdef __cplusplus
 }

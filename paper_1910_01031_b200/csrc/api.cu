@@ -290,6 +290,8 @@ __global__ void count_iters_kernel(const int* sub, int M, unsigned long long* ac
 } // namespace dcg
 
 extern "C" {
+static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream);
+
 
 const char* dc_version(void) { return kVersion; }
 
@@ -312,6 +314,16 @@ dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base
     ctx->use_graph = !(ng && ng[0] == '1');
     derive_params(ctx);
     *out = ctx;
+    dc_status st = dc_create_device(ctx, device, stream);
+    if (st) {
+        std::fprintf(stderr, "dc_create: %s\n", ctx->err.c_str());
+        dc_destroy(ctx);
+        *out = nullptr;
+    }
+    return st;
+}
+
+static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     CU(cudaSetDevice(device));
     if (stream) {
         ctx->stream = static_cast<cudaStream_t>(stream);
@@ -325,7 +337,8 @@ dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base
         CU(cudaMemsetAsync(ctx->f[i], 0, ctx->field_elems * sizeof(float), ctx->stream));
     }
     const int M = ctx->M;
-    size_t bytes = M * (4 * sizeof(double) + 6 * sizeof(int) + 4 * sizeof(unsigned)) + 64;
+    // 11 arrays, each rounded up to 16 bytes by take()
+    size_t bytes = 11 * ((static_cast<size_t>(M) * 4 * sizeof(double) + 15) / 16 * 16) + 64;
     CU(cudaMalloc(&ctx->ctl_mem, bytes));
     CU(cudaMemsetAsync(ctx->ctl_mem, 0, bytes, ctx->stream));
     char* p = static_cast<char*>(ctx->ctl_mem);
@@ -675,6 +688,17 @@ int64_t dc_kernel_launches(dc_ctx* ctx) {
 }
 
 void* dc_stream(dc_ctx* ctx) { return ctx->stream; }
+
+dc_status dc_selftest_math(int32_t device, uint64_t* counts) {
+    if (cudaSetDevice(device) != cudaSuccess) return DC_ECUDA;
+    unsigned long long* d = nullptr;
+    if (cudaMalloc(&d, 4 * sizeof(unsigned long long)) != cudaSuccess) return DC_ECUDA;
+    cudaMemset(d, 0, 4 * sizeof(unsigned long long));
+    launch_selftest_math(nullptr, d);
+    cudaError_t e = cudaMemcpy(counts, d, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? DC_OK : DC_ECUDA;
+}
 
 } // extern "C"
 

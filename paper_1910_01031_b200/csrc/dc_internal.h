@@ -77,6 +77,7 @@ void launch_stage(cudaStream_t s, const SweParams& sp, bool exact, int stage, co
                   const float* s0v, float* oe, float* ou, float* ov, StepCtl ctl);
 void launch_substep_end(cudaStream_t s, const SweParams& sp, StepCtl ctl,
                         unsigned long long cond_handle, int use_cond);
+void launch_selftest_math(cudaStream_t s, unsigned long long* counts);
 void launch_cfl_public(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
                        const float* hv, unsigned long long* gmax, int* dry_pos);
 void launch_flux_rhs(cudaStream_t s, const SweParams& sp, bool exact, int m, const float* eta,
