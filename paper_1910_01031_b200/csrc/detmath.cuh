@@ -174,5 +174,16 @@ __host__ __device__ __forceinline__ int wrapi(int a, int n) {
     return r < 0 ? r + n : r;
 }
 
+// wrap for operands within one period of the range, a in [-n, 2n): no integer division
+__host__ __device__ __forceinline__ int wrap1(int a, int n) {
+    return a < 0 ? a + n : (a >= n ? a - n : a);
+}
+
+// wrap1 with a (rarely taken) exact fallback for tiny periods
+__host__ __device__ __forceinline__ int wrapf(int a, int n) {
+    const int r = wrap1(a, n);
+    return (r < 0 || r >= n) ? wrapi(r, n) : r;
+}
+
 } // namespace det
 } // namespace dcg

@@ -1,0 +1,619 @@
+// iewpf.cu -- observation operators, drifter advection and the two-stage IEWPF analysis
+// on sm_100a (compiled --fmad=false: fp64 expressions follow the restated order exactly).
+//
+// Stage map, all particles at once:
+//   obs_locate      locate_cell of every observation (grid.hpp:55-69), bit-exact fp64
+//   innovations     d = y(H+eta)/H - (hu,hv), S d, phi = sum_o d^T S d in id order, c = phi + log N_e
+//   pull_windows    per (particle, obs): SOAR(SOAR(GB^T dipole(S d))) on the obs-aligned
+//                   coarse grid, kept as an 11x11 window (stochastic.hpp:178-202, 49-69)
+//   tile_lists      per 32x16 fine tile: the observations whose pull footprint covers it
+//   pull_apply      per (particle, tile): for each covering obs in ascending id, Catmull-Rom
+//                   interpolation + geostrophic balance + float-rounded add -- a GATHER
+//                   that reproduces the sequential per-observation add_q_half exactly
+//                   (each cell sees the same ordered sequence of roundings), atomic-free
+//   perp_pair       xi, nu~ (Philox, filter stream), three fixed-order dot products,
+//                   in-place nu transform, gamma, zeta
+//   barrier_alpha   w_target = mean c, beta = min((w-c)/zeta + 1) in particle-id order,
+//                   c*, alpha by Lambert-W Halley iteration
+//   local_blocks    z = beta^1/2 nu + alpha^1/2 xi; 7x7 coarse blocks <- U Sigma^1/2 block,
+//                   ascending obs id
+// then coarse_soar + q_half_apply (stochastic.cu) add P^{1/2} z to the pulled state.
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "dc_internal.h"
+#include "detmath.cuh"
+#include "iewpf_kernels.h"
+
+namespace dcg {
+
+namespace {
+
+using det::wrap1;
+using det::wrapf;
+using det::wrapi;
+
+constexpr int TX = 32, TY = 16;
+constexpr int NBMAX = TY + 2 + 3;
+constexpr int WIN = 11;   // pull window: coarse offsets -5..5
+constexpr int WH = 5;
+
+// locate_cell (grid.hpp:55-69)
+__device__ __forceinline__ bool locate(const SweParams& sp, double x, double y, int* j, int* k) {
+    if (!isfinite(x) || !isfinite(y)) return false;
+    const double lx = sp.nx * sp.dx, ly = sp.ny * sp.dy;
+    double xm = fmod(x, lx);
+    if (xm < 0.0) xm += lx;
+    double ym = fmod(y, ly);
+    if (ym < 0.0) ym += ly;
+    int jj = static_cast<int>(floor(xm / sp.dx));
+    int kk = static_cast<int>(floor(ym / sp.dy));
+    if (jj >= sp.nx) jj = 0;
+    if (kk >= sp.ny) kk = 0;
+    *j = jj;
+    *k = kk;
+    return true;
+}
+
+__global__ void obs_locate_kernel(SweParams sp, const double* __restrict__ obs, int n_obs,
+                                  int* cells, int* bad) {
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < n_obs; o += gridDim.x * blockDim.x) {
+        int j = 0, k = 0;
+        if (!locate(sp, obs[4 * o], obs[4 * o + 1], &j, &k)) atomicExch(bad, 1);
+        cells[2 * o] = j;
+        cells[2 * o + 1] = k;
+    }
+}
+
+// stage 1 + phi/c: one CTA per particle
+__global__ void innovations_kernel(SweParams sp, const float* __restrict__ eta,
+                                   const float* __restrict__ hu, const float* __restrict__ hv,
+                                   const double* __restrict__ obs, const int* __restrict__ cells,
+                                   int n_obs, const double* __restrict__ S, double log_ne,
+                                   double* d, double* sd, double* scal, const int* err) {
+    const int m = blockIdx.x;
+    if (err[m]) return;
+    const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
+    const double S0 = S[0], S1 = S[1], S2 = S[2], S3 = S[3];
+    for (int o = threadIdx.x; o < n_obs; o += blockDim.x) {
+        const int j = cells[2 * o], k = cells[2 * o + 1];
+        const size_t c = mbase + static_cast<size_t>(k) * sp.pitch + j;
+        const double h = sp.h_eq + static_cast<double>(eta[c]);
+        const double d0 = obs[4 * o + 2] * h / sp.h_eq - static_cast<double>(hu[c]);
+        const double d1 = obs[4 * o + 3] * h / sp.h_eq - static_cast<double>(hv[c]);
+        const size_t q = (static_cast<size_t>(m) * n_obs + o) * 2;
+        d[q] = d0;
+        d[q + 1] = d1;
+        sd[q] = S0 * d0 + S1 * d1;
+        sd[q + 1] = S2 * d0 + S3 * d1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double phi = 0.0;
+        for (int o = 0; o < n_obs; ++o) {
+            const size_t q = (static_cast<size_t>(m) * n_obs + o) * 2;
+            phi += d[q] * sd[q] + d[q + 1] * sd[q + 1];
+        }
+        scal[8 * m + 1] = phi;
+        scal[8 * m + 0] = phi + log_ne;
+    }
+}
+
+// SOAR(SOAR(GB^T dipole)) of one (particle, obs) on its aligned coarse grid, as an
+// 11x11 window centred on the obs coarse point (requires nxc, nyc >= 11 so nothing
+// aliases). Sums keep apply_soar's order (db outer, da inner, from 0.0); the exact
+// zeros of the reference's full-grid sums do not change any rounding.
+__global__ void pull_windows_kernel(ErrParams ep, const double* __restrict__ sd, int n_obs,
+                                    double* win, const int* err) {
+    const int m = blockIdx.y, o = blockIdx.x;
+    if (err[m]) return;
+    __shared__ double s1[WIN * WIN];
+    const size_t q = (static_cast<size_t>(m) * n_obs + o) * 2;
+    const double yhu = sd[q], yhv = sd[q + 1];
+    // adjoint_geo_balance values (stochastic.hpp:181-186), accumulated onto 0.0
+    const double vN = 0.0 + (-ep.cyc * yhu);  // (a, b+1)
+    const double vS = 0.0 + (ep.cyc * yhu);   // (a, b-1)
+    const double vE = 0.0 + (ep.cxc * yhv);   // (a+1, b)
+    const double vW = 0.0 + (-ep.cxc * yhv);  // (a-1, b)
+    for (int i = threadIdx.x; i < WIN * WIN; i += blockDim.x) {
+        const int pa = i % WIN - WH, pb = i / WIN - WH;  // offset from the obs point
+        double s = 0.0;
+        for (int db = -2; db <= 2; ++db)
+            for (int da = -2; da <= 2; ++da) {
+                const int ra = pa + da, rb = pb + db;
+                double v = 0.0;
+                if (ra == 0 && rb == 1) v = vN;
+                else if (ra == 0 && rb == -1) v = vS;
+                else if (ra == 1 && rb == 0) v = vE;
+                else if (ra == -1 && rb == 0) v = vW;
+                s += ep.w[(db + 2) * 5 + (da + 2)] * v;
+            }
+        s1[i] = s;
+    }
+    __syncthreads();
+    double* out = win + (static_cast<size_t>(m) * n_obs + o) * (WIN * WIN);
+    for (int i = threadIdx.x; i < WIN * WIN; i += blockDim.x) {
+        const int pa = i % WIN - WH, pb = i / WIN - WH;
+        double s = 0.0;
+        for (int db = -2; db <= 2; ++db)
+            for (int da = -2; da <= 2; ++da) {
+                const int ra = pa + da + WH, rb = pb + db + WH;
+                const double v = (ra >= 0 && ra < WIN && rb >= 0 && rb < WIN) ? s1[rb * WIN + ra] : 0.0;
+                s += ep.w[(db + 2) * 5 + (da + 2)] * v;
+            }
+        out[i] = s;
+    }
+}
+
+// periodic interval [lo, hi] (unwrapped, hi - lo < n) intersects [t0, t1] (t1 < n)?
+__device__ __forceinline__ bool overlaps(int lo, int hi, int t0, int t1, int n) {
+    if (hi - lo + 1 >= n) return true;
+    const int a = wrapi(lo, n);
+    const int b = a + (hi - lo);  // may exceed n-1
+    if (b < n) return !(b < t0 || a > t1);
+    return !(t1 < a && t0 > b - n);  // [a, n-1] U [0, b-n]
+}
+
+// per fine tile: ascending ids of the observations whose pull footprint may touch it
+__global__ void tile_lists_kernel(SweParams sp, ErrParams ep, const int* __restrict__ cells,
+                                  int n_obs, int tiles_x, int n_tiles, int* lists, int* counts) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tiles) return;
+    const int tx = t % tiles_x, ty = t / tiles_x;
+    const int j0 = tx * TX, j1 = min(j0 + TX, sp.nx) - 1;
+    const int k0 = ty * TY, k1 = min(k0 + TY, sp.ny) - 1;
+    const int r = 8 * ep.c + 1;  // footprint radius, generous
+    int n = 0;
+    for (int o = 0; o < n_obs; ++o) {
+        const int jo = cells[2 * o], ko = cells[2 * o + 1];
+        if (overlaps(jo - r, jo + r, j0, j1, sp.nx) && overlaps(ko - r, ko + r, k0, k1, sp.ny))
+            lists[static_cast<size_t>(t) * n_obs + n++] = o;
+    }
+    counts[t] = n;
+}
+
+__device__ __forceinline__ void row_coords(const ErrParams& ep, int kk, int ok, int* b0,
+                                           double* ty) {
+    const double yc = static_cast<double>(kk - ok) * ep.inv_c;
+    *b0 = static_cast<int>(floor(yc));
+    *ty = yc - *b0;
+}
+
+// Sequential-equivalent gather of every covering observation's pull into one tile of one
+// particle (optimal_proposal_pull, SPEC.md:455-463 + add_q_half, stochastic.hpp:144-160).
+__global__ void __launch_bounds__(256)
+pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win,
+                  const int* __restrict__ cells, int n_obs, const int* __restrict__ lists,
+                  const int* __restrict__ counts, int tiles_x, float* eta, float* hu, float* hv,
+                  int* err, int* err_pos) {
+    __shared__ double W[WIN * WIN];
+    __shared__ double X[NBMAX][TX + 2];
+    __shared__ double D[TY + 2][TX + 2];
+    const int m = blockIdx.y;
+    if (err[m]) return;
+    const int tile = blockIdx.x;
+    const int cnt = counts[tile];
+    if (cnt == 0) return;
+    const int j0 = (tile % tiles_x) * TX, k0 = (tile / tiles_x) * TY;
+    const int tid = threadIdx.x;
+    const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
+    // the tile's cells live in registers across all observations (2 per thread)
+    float e[2], u[2], v[2];
+    bool valid[2];
+    size_t off[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int i = tid + q * 256;
+        const int k = k0 + i / TX, j = j0 + i % TX;
+        valid[q] = (k < sp.ny) && (j < sp.nx);
+        off[q] = mbase + static_cast<size_t>(valid[q] ? k : 0) * sp.pitch + (valid[q] ? j : 0);
+        e[q] = valid[q] ? eta[off[q]] : 0.0f;
+        u[q] = valid[q] ? hu[off[q]] : 0.0f;
+        v[q] = valid[q] ? hv[off[q]] : 0.0f;
+    }
+    bool dry = false;
+    int dry_at = 0x7fffffff;
+    for (int li = 0; li < cnt; ++li) {
+        const int o = lists[static_cast<size_t>(tile) * n_obs + li];
+        const int jo = cells[2 * o], ko = cells[2 * o + 1];
+        const int oj = jo % ep.c, ok = ko % ep.c;           // align_coarse_offset
+        const int ao = wrapi((jo - oj) / ep.c, ep.nxc);     // coarse_point_of
+        const int bo = wrapi((ko - ok) / ep.c, ep.nyc);
+        const double* wsrc = win + (static_cast<size_t>(m) * n_obs + o) * (WIN * WIN);
+        __syncthreads();  // previous obs done with W/X/D
+        for (int i = tid; i < WIN * WIN; i += 256) W[i] = wsrc[i];
+        int bfirst, blast;
+        double tdum;
+        row_coords(ep, wrap1(k0 - 1, sp.ny), ok, &bfirst, &tdum);
+        row_coords(ep, wrap1(k0 + TY, sp.ny), ok, &blast, &tdum);
+        const bool whole = ep.nyc <= NBMAX;
+        const int bstart = whole ? 0 : wrapf(bfirst - 1, ep.nyc);
+        const int nb = whole ? ep.nyc : wrapf(blast - bfirst, ep.nyc) + 4;
+        __syncthreads();
+        // coarse value of the window (zero outside): corr(a, b)
+        auto corr = [&](int a, int b) -> double {
+            const int da = wrapf(a - ao + WH, ep.nxc), db = wrapf(b - bo + WH, ep.nyc);
+            return (da < WIN && db < WIN) ? W[db * WIN + da] : 0.0;
+        };
+        for (int i = tid; i < nb * (TX + 2); i += 256) {
+            const int s = i / (TX + 2), jl = i % (TX + 2);
+            const int b = whole ? s : wrap1(bstart + s, ep.nyc);
+            const int jw = wrap1(j0 - 1 + jl, sp.nx);
+            const double xc = static_cast<double>(jw - oj) * ep.inv_c;
+            const int a0 = static_cast<int>(floor(xc));
+            const double tx = xc - a0;
+            X[s][jl] = det::catmull(corr(wrapf(a0 - 1, ep.nxc), b), corr(wrapf(a0, ep.nxc), b),
+                                    corr(wrapf(a0 + 1, ep.nxc), b), corr(wrapf(a0 + 2, ep.nxc), b),
+                                    tx);
+        }
+        __syncthreads();
+        for (int i = tid; i < (TY + 2) * (TX + 2); i += 256) {
+            const int r = i / (TX + 2), jl = i % (TX + 2);
+            const int kk = wrap1(k0 - 1 + r, sp.ny);
+            int b0;
+            double ty;
+            row_coords(ep, kk, ok, &b0, &ty);
+            int sl[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int b = wrapf(b0 - 1 + q, ep.nyc);
+                sl[q] = whole ? b : wrapf(b - bstart, ep.nyc);
+            }
+            D[r][jl] = det::catmull(X[sl[0]][jl], X[sl[1]][jl], X[sl[2]][jl], X[sl[3]][jl], ty);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            if (!valid[q]) continue;
+            const int i = tid + q * 256;
+            const int r = i / TX + 1, jl = i % TX + 1;
+            const double de = D[r][jl];
+            const double dhu = -ep.cy * (D[r + 1][jl] - D[r - 1][jl]);
+            const double dhv = ep.cx * (D[r][jl + 1] - D[r][jl - 1]);
+            const double ee = static_cast<double>(e[q]) + 1.0 * de;
+            if (!(ep.h_eq + ee > 0.0)) {
+                dry = true;
+                dry_at = min(dry_at, (k0 + r - 1) * sp.nx + (j0 + jl - 1));
+            }
+            e[q] = static_cast<float>(ee);
+            u[q] = static_cast<float>(static_cast<double>(u[q]) + 1.0 * dhu);
+            v[q] = static_cast<float>(static_cast<double>(v[q]) + 1.0 * dhv);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+        if (valid[q]) {
+            eta[off[q]] = e[q];
+            hu[off[q]] = u[q];
+            hv[off[q]] = v[q];
+        }
+    if (dry) {
+        atomicCAS(err + m, 0, E_DRY_ADD);
+        atomicMin(err_pos + m, dry_at);
+    }
+}
+
+// Stage 3: perpendicular pair + fixed-order dot products (256 strided partials, then a
+// halving tree -- the order the CPU checker restates). One CTA of 256 per particle.
+__global__ void __launch_bounds__(256)
+perp_pair_kernel(ErrParams ep, uint64_t seed, long long member_base, uint64_t cycle,
+                 double ratio, double* xi, double* nu, int* foffs, double* scal,
+                 const int* err) {
+    const int m = blockIdx.x;
+    if (err[m]) return;
+    const int nr = ep.nxc * ep.nyc;
+    const uint64_t key = det::stream_key(seed, 2 /*filter*/, static_cast<uint64_t>(member_base + m));
+    double* X = xi + static_cast<size_t>(m) * nr;
+    double* N = nu + static_cast<size_t>(m) * nr;
+    const int npairs = (nr + 1) / 2;
+    for (int p = threadIdx.x; p < npairs; p += 256) {
+        double a, b;
+        det::normal_pair(key, 0, cycle, static_cast<uint32_t>(p), &a, &b);
+        X[2 * p] = a;
+        if (2 * p + 1 < nr) X[2 * p + 1] = b;
+        det::normal_pair(key, 1, cycle, static_cast<uint32_t>(p), &a, &b);
+        N[2 * p] = a;
+        if (2 * p + 1 < nr) N[2 * p + 1] = b;
+    }
+    if (threadIdx.x == 0) {
+        int oj, ok;
+        det::draw_offsets(key, 0, cycle, ep.c, &oj, &ok);
+        foffs[2 * m] = oj;
+        foffs[2 * m + 1] = ok;
+    }
+    __syncthreads();
+    __shared__ double pxx[256], pnn[256], pnx[256];
+    const int l = threadIdx.x;
+    double sxx = 0.0, snn = 0.0, snx = 0.0;
+    for (int i = l; i < nr; i += 256) {
+        const double x = X[i], n = N[i];
+        sxx += x * x;
+        snn += n * n;
+        snx += n * x;
+    }
+    pxx[l] = sxx;
+    pnn[l] = snn;
+    pnx[l] = snx;
+    __syncthreads();
+    for (int s = 128; s >= 1; s >>= 1) {
+        if (l < s) {
+            pxx[l] = pxx[l] + pxx[l + s];
+            pnn[l] = pnn[l] + pnn[l + s];
+            pnx[l] = pnx[l] + pnx[l + s];
+        }
+        __syncthreads();
+    }
+    const double xx = pxx[0], nn = pnn[0], nxv = pnx[0];
+    const double a = nxv / xx;
+    const double sc = sqrt(nn / (nn - a * nxv));
+    for (int i = l; i < nr; i += 256) N[i] = sc * (N[i] - a * X[i]);
+    if (l == 0) {
+        scal[8 * m + 2] = xx * ratio;  // gamma
+        scal[8 * m + 3] = nn * ratio;  // zeta
+    }
+}
+
+__global__ void gather_cz_kernel(int M, const double* __restrict__ scal, double* cz) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    cz[2 * m] = scal[8 * m + 0];
+    cz[2 * m + 1] = scal[8 * m + 3];
+}
+
+// Lambert W0 by Halley iteration, fp64, tol 1e-12, clamp within 1e-9 of -1/e
+__device__ bool lambert_w0(double x, double* w_out) {
+    const double em1 = 0.36787944117144233;
+    if (x < -em1) {
+        if (x >= -em1 - 1e-9) x = -em1;
+        else return false;
+    }
+    if (x == -em1) {
+        *w_out = -1.0;
+        return true;
+    }
+    double w;
+    if (x < -0.32) {
+        const double p = sqrt(2.0 * (2.71828182845904509080 * x + 1.0));
+        w = -1.0 + p * (1.0 + p * (-1.0 / 3.0 + p * (11.0 / 72.0)));
+    } else {
+        w = x - x * x;
+    }
+    for (int it = 0; it < 100; ++it) {
+        const double ew = det::exp_det(w);
+        const double f = w * ew - x;
+        const double wp1 = w + 1.0;
+        if (wp1 == 0.0) break;
+        const double den = ew * wp1 - (w + 2.0) * f / (2.0 * wp1);
+        const double dw = f / den;
+        w = w - dw;
+        if (fabs(dw) <= 1e-12 * (1.0 + fabs(w))) {
+            *w_out = w;
+            return true;
+        }
+    }
+    return false;
+}
+
+// Stage 4 (the barrier) + stage 5. Single CTA: the sum for w_target and the beta min
+// run in particle-id order over all N_e particles; every rank computes them identically.
+__global__ void barrier_alpha_kernel(const double* __restrict__ cz_all, int n_total, int M,
+                                     double n_psi, double* scal, double* wb, int* err) {
+    __shared__ double s_w, s_b;
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+        for (int i = 0; i < n_total; ++i) sum += cz_all[2 * i];
+        const double w = sum / n_total;
+        double beta = __longlong_as_double(0x7ff0000000000000ll);
+        int bad = 0;
+        for (int i = 0; i < n_total; ++i) {
+            const double z = cz_all[2 * i + 1];
+            if (!(z > 0.0)) bad = 1;
+            const double b = (w - cz_all[2 * i]) / z + 1.0;
+            beta = (b < beta) ? b : beta;
+        }
+        if (!(beta >= 0.0)) bad = 1;
+        s_w = w;
+        s_b = beta;
+        s_bad = bad;
+        wb[0] = w;
+        wb[1] = beta;
+    }
+    __syncthreads();
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+        if (err[m]) continue;
+        if (s_bad) {
+            atomicCAS(err + m, 0, E_BETA);
+            continue;
+        }
+        const double c = scal[8 * m + 0], gamma = scal[8 * m + 2], zeta = scal[8 * m + 3];
+        const double cstar = (s_w - c) - (s_b - 1.0) * zeta;
+        const double t = gamma / n_psi;
+        const double x = -((t * det::exp_det(-t)) * det::exp_det(-cstar / n_psi));
+        double w;
+        if (!lambert_w0(x, &w)) {
+            atomicCAS(err + m, 0, E_ALPHA);
+            continue;
+        }
+        scal[8 * m + 4] = -(n_psi / gamma) * w;
+    }
+}
+
+// nearest coarse point of fine index j on an offset-o grid
+__device__ __forceinline__ int nearest_coarse(int j, int o, int c, int n) {
+    const int v = j - o + (c - 1) / 2;
+    const int q = (v >= 0) ? v / c : -((-v + c - 1) / c);
+    return wrapi(q, n);
+}
+
+// Stage 6a: z = beta^1/2 nu + alpha^1/2 xi, then the local U Sigma^1/2 blocks in ascending
+// obs id (overlapping blocks see earlier updates, as the sequential restatement does).
+__global__ void __launch_bounds__(64)
+local_blocks_kernel(ErrParams ep, const double* __restrict__ xi, const double* __restrict__ nu,
+                    const double* __restrict__ scal, const double* __restrict__ wb,
+                    const int* __restrict__ cells, int n_obs, const int* __restrict__ foffs,
+                    const double* __restrict__ usig, double* z, const int* err) {
+    const int m = blockIdx.x;
+    if (err[m]) return;
+    __shared__ double U[49 * 49];
+    __shared__ double bin[49];
+    __shared__ int idx[49];
+    const int nr = ep.nxc * ep.nyc;
+    for (int i = threadIdx.x; i < 49 * 49; i += blockDim.x) U[i] = usig[i];
+    const double sqb = sqrt(wb[1]);
+    const double sqa = sqrt(scal[8 * m + 4]);
+    const double* X = xi + static_cast<size_t>(m) * nr;
+    const double* N = nu + static_cast<size_t>(m) * nr;
+    double* Z = z + static_cast<size_t>(m) * nr;
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) Z[i] = sqb * N[i] + sqa * X[i];
+    const int oj = foffs[2 * m], ok = foffs[2 * m + 1];
+    __syncthreads();
+    const int r = threadIdx.x;
+    for (int o = 0; o < n_obs; ++o) {
+        const int a0 = nearest_coarse(cells[2 * o], oj, ep.c, ep.nxc);
+        const int b0 = nearest_coarse(cells[2 * o + 1], ok, ep.c, ep.nyc);
+        if (r < 49) {
+            const int id = wrapf(b0 + r / 7 - 3, ep.nyc) * ep.nxc + wrapf(a0 + r % 7 - 3, ep.nxc);
+            idx[r] = id;
+            bin[r] = Z[id];
+        }
+        __syncthreads();
+        if (r < 49) {
+            double s = 0.0;
+            for (int c = 0; c < 49; ++c) s += U[r * 49 + c] * bin[c];
+            Z[idx[r]] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// advect_drifters: forward Euler at the containing cell, fp64
+__global__ void drifters_kernel(SweParams sp, const float* __restrict__ eta,
+                                const float* __restrict__ hu, const float* __restrict__ hv,
+                                int M, int n_d, double dt, double* pos, int* wind, int* err,
+                                int* err_pos) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M * n_d) return;
+    const int m = i / n_d;
+    if (err[m]) return;
+    double* p = pos + 2 * static_cast<size_t>(i);
+    int j, k;
+    if (!locate(sp, p[0], p[1], &j, &k)) {
+        atomicCAS(err + m, 0, E_DRY_DRIFTER);
+        return;
+    }
+    const size_t c = static_cast<size_t>(m) * sp.ny * sp.pitch + static_cast<size_t>(k) * sp.pitch + j;
+    const double h = sp.h_eq + static_cast<double>(eta[c]);
+    if (!(h > 0.0)) {
+        atomicCAS(err + m, 0, E_DRY_DRIFTER);
+        atomicMin(err_pos + m, k * sp.nx + j);
+        return;
+    }
+    const double u = static_cast<double>(hu[c]) / h;
+    const double v = static_cast<double>(hv[c]) / h;
+    const double lx = sp.nx * sp.dx, ly = sp.ny * sp.dy;
+    const double xs[2] = {p[0] + dt * u, p[1] + dt * v};
+    const double ls[2] = {lx, ly};
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        const double xn = xs[a], len = ls[a];
+        double xm = fmod(xn, len);
+        if (xm < 0.0) xm += len;
+        if (xm >= len) xm = 0.0;
+        wind[2 * static_cast<size_t>(i) + a] += (xn >= len) ? 1 : ((xn < 0.0) ? -1 : 0);
+        p[a] = xm;
+    }
+}
+
+// observe_mooring without noise, one member
+__global__ void observe_mooring_kernel(SweParams sp, const float* __restrict__ eta,
+                                       const float* __restrict__ hu, const float* __restrict__ hv,
+                                       int m, const double* __restrict__ xy, int n, double* y,
+                                       int* bad) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= n) return;
+    int j, k;
+    if (!locate(sp, xy[2 * o], xy[2 * o + 1], &j, &k)) {
+        atomicExch(bad, 1);
+        return;
+    }
+    const size_t c = static_cast<size_t>(m) * sp.ny * sp.pitch + static_cast<size_t>(k) * sp.pitch + j;
+    const double h = sp.h_eq + static_cast<double>(eta[c]);
+    y[2 * o] = static_cast<double>(hu[c]) * sp.h_eq / h;
+    y[2 * o + 1] = static_cast<double>(hv[c]) * sp.h_eq / h;
+}
+
+} // namespace
+
+void launch_obs_locate(cudaStream_t s, const SweParams& sp, const double* obs, int n_obs,
+                       int* cells, int* bad) {
+    obs_locate_kernel<<<(n_obs + 127) / 128, 128, 0, s>>>(sp, obs, n_obs, cells, bad);
+}
+
+void launch_innovations(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
+                        const float* hv, const double* obs, const int* cells, int n_obs,
+                        const double* S, double log_ne, double* d, double* sd, double* scal,
+                        const int* err, int M) {
+    innovations_kernel<<<M, 256, 0, s>>>(sp, eta, hu, hv, obs, cells, n_obs, S, log_ne, d, sd,
+                                          scal, err);
+}
+
+void launch_pull_windows(cudaStream_t s, const ErrParams& ep, const double* sd, int n_obs,
+                         double* win, const int* err, int M) {
+    pull_windows_kernel<<<dim3(n_obs, M), 128, 0, s>>>(ep, sd, n_obs, win, err);
+}
+
+void launch_tile_lists(cudaStream_t s, const SweParams& sp, const ErrParams& ep, const int* cells,
+                       int n_obs, int* lists, int* counts, int* n_tiles_out, int* tiles_x_out) {
+    const int tiles_x = (sp.nx + TX - 1) / TX, tiles_y = (sp.ny + TY - 1) / TY;
+    const int n_tiles = tiles_x * tiles_y;
+    tile_lists_kernel<<<(n_tiles + 127) / 128, 128, 0, s>>>(sp, ep, cells, n_obs, tiles_x, n_tiles,
+                                                           lists, counts);
+    *n_tiles_out = n_tiles;
+    *tiles_x_out = tiles_x;
+}
+
+void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep, const double* win,
+                       const int* cells, int n_obs, const int* lists, const int* counts,
+                       int n_tiles, int tiles_x, float* eta, float* hu, float* hv, int* err,
+                       int* err_pos, int M) {
+    pull_apply_kernel<<<dim3(n_tiles, M), 256, 0, s>>>(sp, ep, win, cells, n_obs, lists, counts,
+                                                       tiles_x, eta, hu, hv, err, err_pos);
+}
+
+void launch_perp_pair(cudaStream_t s, const ErrParams& ep, uint64_t seed, int64_t member_base,
+                      uint64_t cycle, double ratio, double* xi, double* nu, int* foffs,
+                      double* scal, const int* err, int M) {
+    perp_pair_kernel<<<M, 256, 0, s>>>(ep, seed, member_base, cycle, ratio, xi, nu, foffs, scal,
+                                       err);
+}
+
+void launch_gather_cz(cudaStream_t s, int M, const double* scal, double* cz) {
+    gather_cz_kernel<<<(M + 127) / 128, 128, 0, s>>>(M, scal, cz);
+}
+
+void launch_barrier_alpha(cudaStream_t s, const double* cz_all, int n_total, int M, double n_psi,
+                          double* scal, double* wb, int* err) {
+    barrier_alpha_kernel<<<1, 256, 0, s>>>(cz_all, n_total, M, n_psi, scal, wb, err);
+}
+
+void launch_local_blocks(cudaStream_t s, const ErrParams& ep, const double* xi, const double* nu,
+                         const double* scal, const double* wb, const int* cells, int n_obs,
+                         const int* foffs, const double* usig, double* z, const int* err, int M) {
+    local_blocks_kernel<<<M, 64, 0, s>>>(ep, xi, nu, scal, wb, cells, n_obs, foffs, usig, z, err);
+}
+
+void launch_drifters(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
+                     const float* hv, int M, int n_d, double dt, double* pos, int* wind, int* err,
+                     int* err_pos) {
+    const int n = M * n_d;
+    drifters_kernel<<<(n + 127) / 128, 128, 0, s>>>(sp, eta, hu, hv, M, n_d, dt, pos, wind, err,
+                                                    err_pos);
+}
+
+void launch_observe_mooring(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
+                            const float* hv, int m, const double* xy, int n, double* y, int* bad) {
+    observe_mooring_kernel<<<(n + 127) / 128, 128, 0, s>>>(sp, eta, hu, hv, m, xy, n, y, bad);
+}
+
+} // namespace dcg

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <vector>
 
 namespace dcg {
 
@@ -24,6 +25,15 @@ struct IewpfBuffers {
     double* S = nullptr;      // [4]
     double* usig = nullptr;   // [49*49]
     int* foffs = nullptr;     // [M][2] filter-grid offsets
+    double* z = nullptr;      // [M][nr] posterior coarse field
+    int* bad = nullptr;       // locate failure flag
+    int n_total = 0;
+    uint64_t cycle = 0;
+    double S_host[4] = {0, 0, 0, 0};
+    std::vector<double> usig_host;
+    bool usig_valid = false;
+    void* stage = nullptr;    // pinned host staging
+    size_t stage_bytes = 0;
     // drifters
     int n_d = 0;
     double* dpos = nullptr;   // [M][n_d][2]
@@ -32,9 +42,10 @@ struct IewpfBuffers {
 
 inline void iewpf_free(IewpfBuffers& b) {
     void* ps[] = {b.obs, b.cells, b.d, b.sd, b.win, b.tile_lists, b.tile_count, b.nu, b.scal,
-                  b.cz, b.cz_all, b.wb, b.S, b.usig, b.foffs, b.dpos, b.dwind};
+                  b.cz, b.cz_all, b.wb, b.S, b.usig, b.foffs, b.dpos, b.dwind, b.z, b.bad};
     for (void* p : ps)
         if (p) cudaFree(p);
+    if (b.stage) cudaFreeHost(b.stage);
     b = IewpfBuffers{};
 }
 

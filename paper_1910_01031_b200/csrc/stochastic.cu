@@ -24,6 +24,7 @@ namespace dcg {
 
 namespace {
 
+using det::wrap1;
 using det::wrapi;
 
 __global__ void philox_noise_kernel(ErrParams ep, int M, uint64_t seed, uint64_t tag,
@@ -62,10 +63,10 @@ __global__ void coarse_soar_kernel(ErrParams ep, int M, const double* __restrict
         double s = 0.0;
 #pragma unroll
         for (int db = -2; db <= 2; ++db) {
-            const int bb = wrapi(b + db, ep.nyc);
+            const int bb = det::wrapf(b + db, ep.nyc);
 #pragma unroll
             for (int da = -2; da <= 2; ++da)
-                s += ep.w[(db + 2) * 5 + (da + 2)] * __ldg(src + bb * ep.nxc + wrapi(a + da, ep.nxc));
+                s += ep.w[(db + 2) * 5 + (da + 2)] * __ldg(src + bb * ep.nxc + det::wrapf(a + da, ep.nxc));
         }
         out[static_cast<size_t>(m) * nr + i] = s;
     }
@@ -108,29 +109,29 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
     // pass 1: x-interpolation of the needed coarse rows at the tile's fine columns
     for (int i = tid; i < nb * (TX + 2); i += blockDim.x) {
         const int s = i / (TX + 2), jl = i % (TX + 2);
-        const int b = whole ? s : wrapi(bstart + s, ep.nyc);
-        const int jw = wrapi(j0 - 1 + jl, sp.nx);
+        const int b = whole ? s : wrap1(bstart + s, ep.nyc);
+        const int jw = wrap1(j0 - 1 + jl, sp.nx);
         const double xc = static_cast<double>(jw - oj) * ep.inv_c;
         const int a0 = static_cast<int>(floor(xc));
         const double tx = xc - a0;
         const double* row = cf + b * ep.nxc;
-        X[s][jl] = det::catmull(__ldg(row + wrapi(a0 - 1, ep.nxc)), __ldg(row + wrapi(a0, ep.nxc)),
-                                __ldg(row + wrapi(a0 + 1, ep.nxc)), __ldg(row + wrapi(a0 + 2, ep.nxc)),
+        X[s][jl] = det::catmull(__ldg(row + det::wrapf(a0 - 1, ep.nxc)), __ldg(row + det::wrapf(a0, ep.nxc)),
+                                __ldg(row + det::wrapf(a0 + 1, ep.nxc)), __ldg(row + det::wrapf(a0 + 2, ep.nxc)),
                                 tx);
     }
     __syncthreads();
     // pass 2: y-interpolation -> delta eta on the tile + 1-cell halo
     for (int i = tid; i < (TY + 2) * (TX + 2); i += blockDim.x) {
         const int r = i / (TX + 2), jl = i % (TX + 2);
-        const int kk = wrapi(k0 - 1 + r, sp.ny);
+        const int kk = wrap1(k0 - 1 + r, sp.ny);
         int b0;
         double ty;
         row_coords(ep, kk, ok, &b0, &ty);
         int sl[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const int b = wrapi(b0 - 1 + q, ep.nyc);
-            sl[q] = whole ? b : wrapi(b - bstart, ep.nyc);
+            const int b = det::wrapf(b0 - 1 + q, ep.nyc);
+            sl[q] = whole ? b : det::wrapf(b - bstart, ep.nyc);
         }
         D[r][jl] = det::catmull(X[sl[0]][jl], X[sl[1]][jl], X[sl[2]][jl], X[sl[3]][jl], ty);
     }

@@ -1,0 +1,188 @@
+"""GPU parity of the observation system and the two-stage IEWPF analysis (C ABI vs the
+CPU restatement in oracle/). These rows have no reference code;
+the restatement follows SPEC.md/PAPER.md with the spec gaps decided in DESIGN.md §5, and
+the GPU must match it BITWISE: the per-observation pull is a gather that reproduces the
+sequential add_q_half roundings, the dot products use the restated fixed reduction order
+and alpha uses the deterministic exp/log both sides implement.
+"""
+import numpy as np
+import pytest
+
+from checkers import State, make_params
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1910_01031_b200 as pkg
+    return pkg
+
+
+def setup(nx=100, ny=60, n=6, seed=0, **kw):
+    pkg = _gpu()
+    cfg = pkg.Config(nx=nx, ny=ny, **kw)
+    p = make_params(nx=nx, ny=ny, q0=cfg.q0, seed=cfg.seed, c_omega=cfg.c_omega)
+    return pkg, cfg, p
+
+
+def spread_states(oracle, p, n, seed):
+    """Double jet + Philox model error: n distinct members (via the oracle)."""
+    e = np.empty((n, p.ny, p.nx), np.float32)
+    u, v = np.empty_like(e), np.empty_like(e)
+    for m in range(n):
+        s = oracle.init_double_jet(p)
+        for d in range(3):
+            oracle.perturb_philox(p, s, 1000 + m + 37 * seed, d)
+        e[m], u[m], v[m] = s.eta, s.hu, s.hv
+    return e, u, v
+
+
+def obs_set(p, n_obs, seed):
+    rng = np.random.default_rng(seed)
+    lx, ly = p.nx * p.dx, p.ny * p.dy
+    xy = rng.uniform(0, 1, size=(n_obs, 2)) * [lx, ly]
+    xy[0] = [0.3 * p.dx, (p.ny - 0.5) * p.dy]          # near the periodic corner
+    if n_obs > 2:
+        xy[1] = xy[2] + [3 * p.dx, -2 * p.dy]           # overlapping footprints
+    yv = rng.normal(0, 20.0, size=(n_obs, 2))
+    return np.hstack([xy, yv])
+
+
+def test_precompute_S_and_block(oracle):
+    pkg, cfg, p = setup(500, 300)
+    h, S = pkg.precompute_S(cfg)
+    ho, So = oracle.precompute_S(p, 0, 0)
+    assert np.array_equal(h, ho) and np.array_equal(S, So)
+    # SURVEY.md §8a a20 probe: S = 0.881140 I at 500x300 (position independent)
+    assert abs(S[0, 0] - 0.881140) < 5e-6 and abs(S[1, 1] - 0.881140) < 5e-6
+    assert abs(S[0, 1]) < 1e-12
+    blk, usig = pkg.precompute_local_svd(cfg, S)
+    assert np.array_equal(blk, oracle.local_block(p, S))
+    assert np.abs(usig @ usig.T - blk).max() < 1e-12
+    # structure: 45 non-identity rows before corner inclusion
+    nonid = [r for r in range(49) if np.any(np.abs(blk[r] - np.eye(49)[r]) > 0)]
+    corners = {0, 6, 42, 48}
+    assert len([r for r in nonid if r not in corners]) == 45
+
+
+def test_innovations_bitwise(oracle):
+    pkg, cfg, p = setup()
+    n = 4
+    e, u, v = spread_states(oracle, p, n, 1)
+    obs = obs_set(p, 9, 2)
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    d = ens.innovations(obs)
+    for m in range(n):
+        do = oracle.innovations(p, State(e[m], u[m], v[m]), obs)
+        assert np.array_equal(d[m], do)
+
+
+def test_drifters_bitwise(oracle):
+    pkg, cfg, p = setup()
+    n, nd = 3, 17
+    e, u, v = spread_states(oracle, p, n, 3)
+    u += 40.0  # strong eastward transport so drifters cross the periodic edge
+    rng = np.random.default_rng(5)
+    pos = rng.uniform(0, 1, size=(n, nd, 2)) * [p.nx * p.dx, p.ny * p.dy]
+    pos[:, 0] = [p.nx * p.dx - 1.0, 10.0]
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    ens.drifters_set(pos)
+    for _ in range(7):
+        ens.advect_drifters(60.0)
+    gp, gw = ens.drifters_get()
+    for m in range(n):
+        q = pos[m].copy()
+        w = np.zeros((nd, 2), np.int32)
+        s = State(e[m], u[m], v[m])
+        for _ in range(7):
+            oracle.advect_drifters(p, s, q, 60.0, w)
+        assert np.array_equal(gp[m], q)
+        assert np.array_equal(gw[m], w)
+    assert gw[:, 0, 0].min() >= 1  # the edge drifter wrapped
+
+
+@pytest.mark.parametrize("nx,ny,n,n_obs", [(100, 60, 6, 7), (500, 300, 4, 24)])
+def test_iewpf_assimilate_bitwise(oracle, nx, ny, n, n_obs):
+    pkg, cfg, p = setup(nx, ny)
+    e, u, v = spread_states(oracle, p, n, 7)
+    obs = obs_set(p, n_obs, 11)
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S) + 0.0 * np.eye(49))
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    ens.iewpf_assimilate(obs, S, usig, cycle=3)
+    ge, gu, gv, _ = ens.download()
+    diag, wb = ens.iewpf_diagnostics()
+    oe, ou, ov = e.copy(), u.copy(), v.copy()
+    od, owb = oracle.iewpf_assimilate(p, oe, ou, ov, obs, S, usig, 3)
+    assert np.array_equal(wb, owb), (wb, owb)
+    assert np.array_equal(diag, od), np.abs(diag - od).max(axis=0)
+    for m in range(n):
+        assert np.array_equal(ge[m], oe[m]), (m, np.abs(ge[m] - oe[m]).max())
+        assert np.array_equal(gu[m], ou[m])
+        assert np.array_equal(gv[m], ov[m])
+    assert np.all((diag[:, 4] > 0) & (diag[:, 4] <= 1.0 + 1e-12))
+
+
+def test_iewpf_two_slices_equal_one(oracle):
+    """The multi-GPU decomposition on one device: two contexts own members [0,3) and
+    [3,6); stages 1-3 run per slice, the (c, zeta) pairs are concatenated (the NCCL
+    all-gather), stages 4-6 run per slice. Result == single-context run, bitwise."""
+    pkg, cfg, p = setup()
+    n = 6
+    e, u, v = spread_states(oracle, p, n, 9)
+    obs = obs_set(p, 5, 13)
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    one = pkg.Ensemble(cfg, n)
+    one.upload(e, u, v, 0.0)
+    one.iewpf_assimilate(obs, S, usig, cycle=1)
+    ref = one.download()
+    a = pkg.Ensemble(cfg, 3, member_base=0)
+    b = pkg.Ensemble(cfg, 3, member_base=3)
+    a.upload(e[:3], u[:3], v[:3], 0.0)
+    b.upload(e[3:], u[3:], v[3:], 0.0)
+    cza = a.iewpf_begin(obs, S, usig, 1, n_total=n)
+    czb = b.iewpf_begin(obs, S, usig, 1, n_total=n)
+    cz = np.concatenate([cza, czb])
+    a.iewpf_finish(cz)
+    b.iewpf_finish(cz)
+    ra, rb = a.download(), b.download()
+    for f in range(3):
+        assert np.array_equal(np.concatenate([ra[f], rb[f]]), ref[f])
+
+
+def test_da_cycle_matches_oracle(oracle):
+    """One DA cycle: 5 model steps, Philox model error after the first
+    4, drifters advected each step, then the analysis -- bitwise vs the oracle."""
+    pkg, cfg, p = setup()
+    n = 4
+    e, u, v = spread_states(oracle, p, n, 15)
+    obs = obs_set(p, 6, 17)
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    pos = np.random.default_rng(3).uniform(0, 1, size=(n, 5, 2)) * [p.nx * p.dx, p.ny * p.dy]
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    ens.drifters_set(pos)
+    ens.da_cycle(5, obs, S, usig, cycle=0)
+    ge, gu, gv, gt = ens.download()
+    gp, _ = ens.drifters_get()
+    oe, ou, ov = e.copy(), u.copy(), v.copy()
+    op = pos.copy()
+    for m in range(n):
+        s = State(oe[m], ou[m], ov[m], 0.0)
+        for i in range(5):
+            oracle.advect_drifters(p, s, op[m], 60.0)
+            oracle.model_step(p, s, 1)
+            if i < 4:
+                oracle.perturb_philox(p, s, m, i)
+    oracle.iewpf_assimilate(p, oe, ou, ov, obs, S, usig, 0)
+    assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
+    assert np.array_equal(gp, op)
+    assert np.all(gt == 300.0)
