@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""bench.py -- IEWPF data-assimilation cycle throughput on B200 (driver contract).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on for one GPU):
+double-jet ensemble, 500x300 cells (dx=dy=2220 m), 100 members per GPU, 64 drifter
+observations every 5 min. One bench "step" = one full IEWPF cycle:
+5 model steps of 60 s (CFL substeps on the device), Philox model error after the first
+4, drifters advected in every member each step, then the two-stage IEWPF analysis.
+
+  value  = ensemble cell-updates/s (one cell of one member through one SSP-RK2
+           substep), device-timed with CUDA events over K cycles, state resident in HBM
+  e2e    = the same metric through the C ABI with host buffers: the cycle's observation
+           records copied host->device inside the call, and per-particle diagnostics +
+           drifter positions read back device->host every cycle, wall-clock timed
+  N > 1  = one process per GPU (torchrun), 100 members per rank (weak scaling); the
+           only collective is the NCCL all-gather of (c_i, zeta_i) at the IEWPF barrier.
+
+--impl reference times the reference's own CPU operators (oracle/_ref, compiled from
+/root/reference headers: Stepper::model_step + perturb_state, threaded over all host
+cores) plus this repo's CPU restatement of the analysis (no reference code exists for
+it), on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ensemble cell-updates/s (IEWPF DA cycle)"
+UNIT = "cell-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--members", type=int, default=100, help="members per GPU")
+    ap.add_argument("--nx", type=int, default=500)
+    ap.add_argument("--ny", type=int, default=300)
+    ap.add_argument("--obs", default="drifters", choices=["drifters", "moorings"])
+    ap.add_argument("--fast", action="store_true", help="FMA build of the stencil")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def platforms(cfg, kind):
+    """Observation platforms: 64 drifters on an 8x8 lattice or 240 moorings on 12x20,
+    25 cells apart where the grid allows."""
+    lx, ly = cfg.nx * cfg.dx, cfg.ny * cfg.dy
+    if kind == "moorings":
+        nxp, nyp = 20, 12
+    else:
+        nxp, nyp = 8, 8
+    xs = (np.arange(nxp) + 0.5) / nxp * lx
+    ys = (np.arange(nyp) + 0.5) / nyp * ly
+    X, Y = np.meshgrid(xs, ys)
+    return np.stack([X.ravel(), Y.ravel()], axis=1)
+
+
+def synthetic_observations(pkg, cfg, n_cycles, kind, device, stream):
+    """Twin-experiment truth on the GPU: one member on its own stream family (global id
+    10^6), stepped cycle by cycle with model error; drifters advected in the truth;
+    observations y = H_eq*(hu,hv)/(H_eq+eta) at each platform (observe_mooring,
+    SPEC.md:353-361) + N(0, R=I). Returns [n_cycles][n_obs][4] (x, y, y_hu, y_hv)."""
+    truth = pkg.Ensemble(cfg, 1, member_base=10**6, device=device, stream=stream)
+    truth.init_double_jet()
+    pos = platforms(cfg, kind)
+    moving = kind == "drifters"
+    if moving:
+        truth.drifters_set(pos[None])
+    rng = np.random.default_rng(2024)
+    out = []
+    for _ in range(n_cycles):
+        truth.da_cycle(5, np.zeros((0, 4)), np.eye(2), np.eye(49), 0)
+        if moving:
+            p, _ = truth.drifters_get()
+            pos = p[0]
+        y = truth.observe_mooring(0, pos) + rng.normal(0.0, 1.0, size=(len(pos), 2))
+        out.append(np.hstack([pos, y]))
+    truth.close()
+    return np.array(out)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.p = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)),
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": float(max(power)) if power else None}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic():
+    """dram bytes per SWE stage launch from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "swe_stage_traffic.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_reference_sample(cfg_params, obs, n_members, threads, base_state):
+    """The reference's CPU forecast (Stepper::model_step + perturb_state, threaded) for a
+    bounded member sample + the restated analysis on that sample. Returns
+    (seconds, cell-updates)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from checkers import Oracle, Ref, State, have_ref
+    p = cfg_params
+    orc = Oracle()
+    n = p.nx * p.ny
+    e = np.repeat(base_state.eta[None], n_members, 0).copy()
+    u = np.repeat(base_state.hu[None], n_members, 0).copy()
+    v = np.repeat(base_state.hv[None], n_members, 0).copy()
+    pa = np.array([1, 1, 1, 1, 0], np.uint8)
+    # substeps of one model step (identical across members for the jet at this horizon)
+    s0 = State(e[0].copy(), u[0].copy(), v[0].copy())
+    if have_ref():
+        ref = Ref()
+        subs = len(ref.model_step_dts(p, s0))
+        t0 = time.perf_counter()
+        ref.forecast_threads(p, e, u, v, 5, pa, threads)
+        kind = "reference"
+    else:
+        subs = len(orc.model_step(p, s0, 1))
+        t0 = time.perf_counter()
+        for m in range(n_members):
+            s = State(e[m], u[m], v[m])
+            for k in range(5):
+                orc.model_step(p, s, 1)
+                if k < 4:
+                    orc.perturb_philox(p, s, m, k)
+        kind = "port"
+    _, S = orc.precompute_S(p)
+    usig = np.linalg.cholesky(orc.local_block(p, S))
+    # analysis: member slices on all threads (ctypes releases the GIL); each slice runs
+    # the full six stages, so the work equals one N_e = n_members analysis
+    per = max(1, (n_members + threads - 1) // threads)
+    jobs = []
+    for lo in range(0, n_members, per):
+        hi = min(n_members, lo + per)
+        jobs.append(threading.Thread(target=orc.iewpf_assimilate,
+                                     args=(p, e[lo:hi], u[lo:hi], v[lo:hi], obs, S, usig, 0),
+                                     kwargs={"member_base": lo}))
+    for j in jobs:
+        j.start()
+    for j in jobs:
+        j.join()
+    dt = time.perf_counter() - t0
+    return dt, n_members * 5 * subs * n, kind
+
+
+def run_reference(args, rank, world):
+    """--impl reference: rank 0 times the CPU reference on a bounded sample per step."""
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from checkers import Oracle, make_params
+    p = make_params(nx=args.nx, ny=args.ny)
+    threads = os.cpu_count() or 1
+    sample = max(2, threads)
+    orc = Oracle()
+    base = orc.init_double_jet(p)
+    rng = np.random.default_rng(0)
+    pos = platforms(type("c", (), {"nx": p.nx, "ny": p.ny, "dx": p.dx, "dy": p.dy}), args.obs)
+    obs = np.hstack([pos, rng.normal(0, 20, size=(len(pos), 2))])
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_reference_sample(p, obs, sample, threads, base)
+    times, cus, kind = [], 0, "reference"
+    for _ in range(args.steps):
+        dt, cu, kind = cpu_reference_sample(p, obs, sample, threads, base)
+        times.append(dt)
+        cus = cu
+    med = float(np.median(times))
+    val = cus / med
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 state / f64 covariance", "data": "synthetic",
+        "config": {"workload": "configs[1]: double jet 500x300, IEWPF cycle (5 model steps, "
+                               "4 model-error draws, 64 drifter obs)",
+                   "members_sampled": sample, "nx": p.nx, "ny": p.ny},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{sample} members x 1 IEWPF cycle per step (forecast via "
+                                   f"the reference operators, analysis via the CPU "
+                                   f"restatement; both on {threads} threads)"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist  # noqa: F401  (ranks other than 0 just exit)
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import paper_1910_01031_b200 as pkg
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    cfg = pkg.Config(nx=args.nx, ny=args.ny, exact_fp=not args.fast)
+    M = args.members
+    K, W = args.steps, args.warmup
+    total = M * world
+    with torch.cuda.stream(stream):
+        obs_all = synthetic_observations(pkg, cfg, W + 2 * K + 1, args.obs, local, stream.cuda_stream)
+        _, S = pkg.precompute_S(cfg)
+        _, usig = pkg.precompute_local_svd(cfg, S)
+        ens = pkg.Ensemble(cfg, M, member_base=rank * M, device=local, stream=stream.cuda_stream)
+        ens.init_double_jet()
+        drift0 = platforms(cfg, "drifters")
+        ens.drifters_set(drift0[None].repeat(M, 0))
+        cz_local = torch.zeros((M, 2), dtype=torch.float64, device=f"cuda:{local}")
+        cz_all = torch.zeros((total, 2), dtype=torch.float64, device=f"cuda:{local}")
+
+        def cycle(c):
+            obs = obs_all[c]
+            if world == 1:
+                ens.da_cycle(5, obs, S, usig, c)
+            else:
+                ens.da_cycle(5, np.zeros((0, 4)), S, usig, c)  # forecast + drifters only
+                ens.iewpf_begin(obs, S, usig, c, total, cz_ptr=cz_local.data_ptr())
+                dist.all_gather_into_tensor(cz_all, cz_local)
+                ens.iewpf_finish(cz_ptr=cz_all.data_ptr())
+
+        for c in range(W):
+            cycle(c)
+        ens.sync()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        l0, cs0, _ = ens.counters()
+        clk = ClockSampler(local)
+        clk.start()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ev0.record(stream)
+        for c in range(W, W + K):
+            cycle(c)
+        ev1.record(stream)
+        ev1.synchronize()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        clocks = clk.stop()
+        ms = ev0.elapsed_time(ev1)
+        l1, cs1, _ = ens.counters()
+        ens.sync()
+        cell_updates = (cs1 - cs0) * cfg.nx * cfg.ny
+        if dist:
+            t = torch.tensor([ms, float(cell_updates)], dtype=torch.float64, device=f"cuda:{local}")
+            tmax = t.clone()
+            dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+            ms = float(tmax[0])
+            cell_updates = float(t[1])
+        value = cell_updates / (ms / 1e3)
+
+        # ---- end to end through the C ABI with host buffers ----
+        diag_bytes = M * 40 + 16
+        drift_bytes = M * len(drift0) * 2 * (8 + 4)
+        obs_bytes = obs_all.shape[1] * 32
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2e_cu0 = ens.counters()[1]
+        for c in range(W + K, W + 2 * K):
+            cycle(c)
+            ens.iewpf_diagnostics()    # D2H per-particle (c, phi, gamma, zeta, alpha) + (w, beta)
+            ens.drifters_get()         # D2H forecast drifter ensemble
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e2e_cu = (ens.counters()[1] - e2e_cu0) * cfg.nx * cfg.ny
+        if dist:
+            t = torch.tensor([wall, float(e2e_cu)], dtype=torch.float64, device=f"cuda:{local}")
+            tmax = t.clone()
+            dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+            wall, e2e_cu = float(tmax[0]), float(t[1])
+        e2e_value = e2e_cu / wall
+
+        # ---- roofline of the dominant kernel (SWE stage), CUDA events per launch ----
+        ms1, ms2 = ens.time_stages(7)
+        cells = M * cfg.nx * cfg.ny
+        bytes1, bytes2 = 24.0 * cells, 36.0 * cells  # algorithmic (60 B/cell-update)
+        achieved = (bytes1 + bytes2) / ((ms1 + ms2) / 1e3) / 1e9
+        peaks, peak_src = load_peaks()
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        traffic = profiled_traffic()
+        ens.sync()
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from checkers import Oracle, make_params
+            p = make_params(nx=cfg.nx, ny=cfg.ny)
+            threads = os.cpu_count() or 1
+            sample = max(2, min(threads, 16))
+            base = Oracle().init_double_jet(p)
+            dt, cu, kind = cpu_reference_sample(p, obs_all[0], sample, threads, base)
+            cpu = {"value": cu / dt, "unit": UNIT, "cores": threads, "kind": kind,
+                   "sample": f"{sample} members x 1 IEWPF cycle (5 model steps, 4 perturbs, "
+                             f"{obs_all.shape[1]} obs): forecast on the reference operators "
+                             f"over {threads} threads, analysis via the CPU restatement"}
+        except Exception as ex:  # the checker is optional on the box; never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "unavailable",
+                   "sample": f"{type(ex).__name__}: {ex}"}
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": ms / K,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 state (SWE stencil) / f64 covariance + filter scalars",
+        "data": "synthetic: double-jet IC, Philox model error, twin-experiment truth with "
+                f"{obs_all.shape[1]} {args.obs}, R=I",
+        "config": {"workload": "configs[1]: double-jet IEWPF, 100 members/GPU, 64 drifter obs "
+                               "every 5 min, drifter forecast copies in every member",
+                   "nx": cfg.nx, "ny": cfg.ny, "members_per_gpu": M, "members_total": total,
+                   "n_obs": int(obs_all.shape[1]), "obs": args.obs, "cycle": "5 x 60 s steps, "
+                   "model error after 4, IEWPF analysis", "exact_fp": not args.fast,
+                   "parallelism": f"ensemble dp{world}",
+                   "l2": "inputs larger than L2 (state 3 x 100 x 300 x 512 x 4 B x 2 = 368 MB)"},
+        "cycle_ms": ms / K,
+        "cell_model_steps_per_s": value / max(1.0, cell_updates / (K * 5 * total * cfg.nx * cfg.ny)),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": obs_bytes,
+                "d2h_bytes_per_step": diag_bytes + drift_bytes, "ms_per_step": wall * 1e3 / K},
+        "gpu_launches": int(l1 - l0),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "swe_stage (SSP-RK2 stage, 24 B/cell stage 1, 36 B/cell stage 2)",
+                     "stage_ms": [ms1, ms2], "peak_source": peak_src,
+                     "note": "the stage kernel is FP32-issue bound (SURVEY.md §7); see "
+                             "profiles/ for issue-slot SOL"},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -167,6 +167,13 @@ dc_status dc_da_cycle(dc_ctx* ctx, int32_t n_steps, const dc_obs* obs, int32_t n
 /* ---- instrumentation ------------------------------------------------------------ */
 /* number of kernels this context has launched (host-side counter). */
 int64_t dc_kernel_launches(dc_ctx* ctx);
+/* counters since creation (synchronous): [0] kernels launched, [1] member-substeps
+ * (cell-updates / (nx*ny)), [2] substep-loop iterations. */
+dc_status dc_counters(dc_ctx* ctx, uint64_t* out);
+/* instrumentation for the roofline: n_substeps substeps launched one by one with CUDA
+ * events around each stage kernel; ms_out[0..1] = mean stage-1 / stage-2 duration.
+ * Advances the state (n_substeps substeps of a model step). */
+dc_status dc_time_stages(dc_ctx* ctx, int32_t n_substeps, double* ms_out);
 /* the cudaStream_t the context runs on. */
 void* dc_stream(dc_ctx* ctx);
 /* Exhaustive device self-check of the branch-free IEEE sqrt / reciprocal used by the

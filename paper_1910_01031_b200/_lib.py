@@ -53,7 +53,7 @@ EXPORTS = [
     "dc_innovations", "dc_observe_mooring", "dc_drifters_set", "dc_drifters_advect",
     "dc_drifters_get", "dc_precompute_S", "dc_precompute_local_svd", "dc_iewpf_begin",
     "dc_iewpf_finish", "dc_iewpf_assimilate", "dc_iewpf_diagnostics", "dc_da_cycle",
-    "dc_kernel_launches", "dc_stream", "dc_selftest_math",
+    "dc_kernel_launches", "dc_stream", "dc_selftest_math", "dc_counters", "dc_time_stages",
 ]
 
 
@@ -116,6 +116,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "dc_kernel_launches": (C.c_int64, [vp]),
         "dc_stream": (vp, [vp]),
         "dc_selftest_math": (st, [C.c_int32, C.POINTER(C.c_uint64)]),
+        "dc_counters": (st, [vp, C.POINTER(C.c_uint64)]),
+        "dc_time_stages": (st, [vp, C.c_int32, dp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -32,7 +32,8 @@ struct dc_ctx {
     float* f[6] = {nullptr};  // eta, hu, hv, stage eta, stage hu, stage hv
     StepCtl ctl{};
     void* ctl_mem = nullptr;
-    unsigned long long* substep_iters = nullptr; // device counter (graph path)
+    unsigned long long* substep_iters = nullptr; // device counters (graph path): [iters, member-substeps]
+    unsigned long long* host_iters = nullptr;    // same counters for the host-loop path
     double* xi = nullptr;
     double* corr = nullptr;
     int* offs = nullptr;
@@ -51,6 +52,10 @@ struct dc_ctx {
     std::string err;
     int em = -1, ej = -1, ek = -1, esub = -1;
 };
+
+namespace dcg {
+__global__ void count_iters_kernel(const int* sub, int M, unsigned long long* acc);
+}
 
 namespace {
 
@@ -267,6 +272,8 @@ dc_status step_host_loop(dc_ctx* ctx) {
         guess = 1;
     }
     ctx->last_max_sub = std::max(1, done);
+    count_iters_kernel<<<1, 1024, 0, s>>>(ctx->ctl.sub, ctx->M, ctx->host_iters);
+    ctx->launches += 1;
     return DC_OK;
 }
 
@@ -275,16 +282,30 @@ dc_status step_host_loop(dc_ctx* ctx) {
 // small helper kernel: substep iteration counter for launch accounting
 namespace dcg {
 __global__ void count_iters_kernel(const int* sub, int M, unsigned long long* acc) {
-    unsigned long long mx = 0;
-    for (int m = threadIdx.x; m < M; m += blockDim.x) mx = max(mx, (unsigned long long)sub[m]);
-    for (int off = 16; off > 0; off >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    __shared__ unsigned long long w[32];
-    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = mx;
+    // acc[0] += max_m sub[m] (while-loop iterations), acc[1] += sum_m sub[m] (member-substeps)
+    unsigned long long mx = 0, sm = 0;
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+        mx = max(mx, (unsigned long long)sub[m]);
+        sm += (unsigned long long)sub[m];
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        sm += __shfl_xor_sync(0xffffffffu, sm, off);
+    }
+    __shared__ unsigned long long w[32], v[32];
+    if ((threadIdx.x & 31) == 0) {
+        w[threadIdx.x >> 5] = mx;
+        v[threadIdx.x >> 5] = sm;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long r = 0;
-        for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) r = max(r, w[i]);
-        *acc += r;
+        unsigned long long r = 0, q = 0;
+        for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) {
+            r = max(r, w[i]);
+            q += v[i];
+        }
+        acc[0] += r;
+        acc[1] += q;
     }
 }
 } // namespace dcg
@@ -358,8 +379,10 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     ctx->ctl.err_sub = reinterpret_cast<int*>(take(M * sizeof(int)));
     ctx->ctl.mx = reinterpret_cast<unsigned*>(take(4 * M * sizeof(unsigned)));
     ctx->ctl.any_active = reinterpret_cast<int*>(take(sizeof(int)));
-    CU(cudaMalloc(&ctx->substep_iters, sizeof(unsigned long long)));
-    CU(cudaMemsetAsync(ctx->substep_iters, 0, sizeof(unsigned long long), ctx->stream));
+    CU(cudaMalloc(&ctx->substep_iters, 2 * sizeof(unsigned long long)));
+    CU(cudaMalloc(&ctx->host_iters, 2 * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(ctx->host_iters, 0, 2 * sizeof(unsigned long long), ctx->stream));
+    CU(cudaMemsetAsync(ctx->substep_iters, 0, 2 * sizeof(unsigned long long), ctx->stream));
     // accumulators: max fields 0, min field all-ones (ordered +inf side), err_pos INT_MAX
     std::vector<unsigned> mx(4 * M);
     for (int m = 0; m < M; ++m) {
@@ -389,6 +412,7 @@ dc_status dc_destroy(dc_ctx* ctx) {
     for (auto* q : ctx->f) cudaFree(q);
     cudaFree(ctx->ctl_mem);
     cudaFree(ctx->substep_iters);
+    cudaFree(ctx->host_iters);
     cudaFree(ctx->xi);
     cudaFree(ctx->corr);
     cudaFree(ctx->offs);
@@ -688,6 +712,49 @@ int64_t dc_kernel_launches(dc_ctx* ctx) {
 }
 
 void* dc_stream(dc_ctx* ctx) { return ctx->stream; }
+
+dc_status dc_counters(dc_ctx* ctx, uint64_t* out) {
+    unsigned long long g[2] = {0, 0}, h[2] = {0, 0};
+    CU(cudaMemcpyAsync(g, ctx->substep_iters, sizeof(g), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(h, ctx->host_iters, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    out[0] = static_cast<uint64_t>(dc_kernel_launches(ctx));
+    out[1] = g[1] + h[1];  // member-substeps since creation
+    out[2] = g[0] + h[0];  // substep-loop iterations since creation
+    return DC_OK;
+}
+
+dc_status dc_time_stages(dc_ctx* ctx, int32_t n_substeps, double* ms_out) {
+    // One model step's worth of substeps launched individually with CUDA events around
+    // each stage kernel on the context stream (advances the state like dc_step).
+    cudaStream_t s = ctx->stream;
+    cudaEvent_t ev[3];
+    for (auto& e : ev) CU(cudaEventCreate(&e));
+    launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+    launch_step_begin(s, ctx->sp, ctx->ctl);
+    double t1 = 0.0, t2 = 0.0;
+    for (int i = 0; i < n_substeps; ++i) {
+        CU(cudaEventRecord(ev[0], s));
+        launch_stage(s, ctx->sp, ctx->exact, 1, ctx->f[0], ctx->f[1], ctx->f[2], nullptr, nullptr,
+                     nullptr, ctx->f[3], ctx->f[4], ctx->f[5], ctx->ctl);
+        CU(cudaEventRecord(ev[1], s));
+        launch_stage(s, ctx->sp, ctx->exact, 2, ctx->f[3], ctx->f[4], ctx->f[5], ctx->f[0],
+                     ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+        CU(cudaEventRecord(ev[2], s));
+        launch_substep_end(s, ctx->sp, ctx->ctl, 0ull, 0);
+        CU(cudaEventSynchronize(ev[2]));
+        float a = 0.f, b = 0.f;
+        CU(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        CU(cudaEventElapsedTime(&b, ev[1], ev[2]));
+        t1 += a;
+        t2 += b;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    ctx->launches += 2 + 3 * n_substeps;
+    ms_out[0] = t1 / n_substeps;
+    ms_out[1] = t2 / n_substeps;
+    return surface_errors(ctx);
+}
 
 dc_status dc_selftest_math(int32_t device, uint64_t* counts) {
     if (cudaSetDevice(device) != cudaSuccess) return DC_ECUDA;

@@ -114,6 +114,18 @@ class Ensemble:
     def kernel_launches(self) -> int:
         return int(self.L.dc_kernel_launches(self.h))
 
+    def counters(self):
+        """(kernels launched, member-substeps, substep-loop iterations) since creation."""
+        out = (C.c_uint64 * 3)()
+        self._ck(self.L.dc_counters(self.h, out))
+        return int(out[0]), int(out[1]), int(out[2])
+
+    def time_stages(self, n_substeps=7):
+        """Mean CUDA-event duration (ms) of the stage-1 / stage-2 SWE kernels."""
+        out = np.zeros(2, np.float64)
+        self._ck(self.L.dc_time_stages(self.h, n_substeps, _d(out)))
+        return float(out[0]), float(out[1])
+
     # ---- state I/O ----
     def upload(self, eta, hu, hv, t=None):
         eta, hu, hv = (np.ascontiguousarray(a, np.float32) for a in (eta, hu, hv))
