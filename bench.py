@@ -42,7 +42,7 @@ UNIT = "cell-updates/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--members", type=int, default=100, help="members per GPU")
@@ -115,7 +115,7 @@ class ClockSampler:
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -305,6 +305,8 @@ def main():
                 dist.all_gather_into_tensor(cz_all, cz_local)
                 ens.iewpf_finish(cz_ptr=cz_all.data_ptr())
 
+        clk = ClockSampler(local)
+        clk.start()
         for c in range(W):
             cycle(c)
         ens.sync()
@@ -312,8 +314,6 @@ def main():
         if dist:
             dist.barrier()
         l0, cs0, _ = ens.counters()
-        clk = ClockSampler(local)
-        clk.start()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -327,7 +327,6 @@ def main():
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        clocks = clk.stop()
         ms = ev0.elapsed_time(ev1)
         l1, cs1, _ = ens.counters()
         ens.sync()
@@ -363,6 +362,7 @@ def main():
             dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
             wall, e2e_cu = float(tmax[0]), float(t[1])
         e2e_value = e2e_cu / wall
+        clocks = clk.stop()  # sampled from warm-up through the timed and e2e regions
 
         # ---- roofline of the dominant kernel (SWE stage), CUDA events per launch ----
         ms1, ms2 = ens.time_stages(7)
