@@ -1151,6 +1151,18 @@ int orc_iewpf_assimilate(const orc_params* p, int n_local, uint64_t member_base,
         gam[i] = xx * ratio;
         zet[i] = nn * ratio;
     }
+    // stages 1-3 only (a rank's half of a multi-rank analysis): report the slice's
+    // (c, phi, gamma, zeta) and stop before the barrier. The state keeps the pulls.
+    if (!c_all && n_total != n_local) {
+        for (int i = 0; i < n_local && diag; ++i) {
+            diag[5 * i + 0] = cvec[i];
+            diag[5 * i + 1] = phis[i];
+            diag[5 * i + 2] = gam[i];
+            diag[5 * i + 3] = zet[i];
+            diag[5 * i + 4] = std::numeric_limits<double>::quiet_NaN();
+        }
+        return O_OK;
+    }
     // stage 4: barrier -- w_target = mean c, beta = min((w-c)/zeta + 1), id order
     const double* call = c_all ? c_all : cvec.data();
     const double* zall = zeta_all ? zeta_all : zet.data();
