@@ -1,0 +1,165 @@
+// driftcast_gpu.hpp -- header-only C++ face of the C ABI (driftcast_gpu.h) shaped like
+// the reference operator surface (proj/include/driftcast/*.hpp), for the existing C++
+// driver. Status codes become the reference's exception types:
+//   DC_EINVAL -> std::invalid_argument, DC_EDRY -> DryCellError (swe.hpp:32-34),
+//   DC_ENONFINITE / DC_ERUNAWAY -> std::runtime_error (swe.hpp:255-256, 416-418).
+// When the reference headers are on the include path, driftcast::DryCellError itself is
+// thrown, so existing catch sites keep working unchanged.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "driftcast_gpu.h"
+
+#if defined(__has_include)
+#if __has_include("driftcast/swe.hpp")
+#include "driftcast/swe.hpp"
+#define DRIFTCAST_GPU_HAVE_REFERENCE 1
+#endif
+#endif
+
+namespace driftcast {
+namespace gpu {
+
+#ifdef DRIFTCAST_GPU_HAVE_REFERENCE
+using DryCellError = ::driftcast::DryCellError;
+#else
+struct DryCellError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+#endif
+
+inline void throw_status(dc_status st, const std::string& msg) {
+    switch (st) {
+    case DC_OK: return;
+    case DC_EINVAL: throw std::invalid_argument(msg);
+    case DC_EDRY: throw DryCellError(msg);
+    case DC_ENONFINITE:
+    case DC_ERUNAWAY: throw std::runtime_error(msg);
+    default: throw std::runtime_error("driftcast_gpu: " + msg);
+    }
+}
+
+/// Paper defaults (§5): 500x300 double jet, dx=dy=2220 m, c_Omega=5,
+/// L0 = 3/4 coarse spacing, q0 = 2.5e-4, Courant 0.8, theta 1.3, model dt 60 s.
+inline dc_config default_config() {
+    dc_config c{};
+    c.nx = 500;
+    c.ny = 300;
+    c.dx = c.dy = 2220.0;
+    c.g = 9.806;
+    c.f = 1.405e-4;
+    c.h_eq = 230.0;
+    c.courant = 0.8;
+    c.limiter_theta = 1.3;
+    c.model_dt = 60.0;
+    c.q0 = 2.5e-4;
+    c.c_omega = 5;
+    c.l0 = 0.75 * c.c_omega * c.dx;
+    c.c_soar = 2;
+    c.seed = 1;
+    c.exact_fp = 1;
+    return c;
+}
+
+/// Precomputed IEWPF operators.
+struct FilterOperators {
+    double hqht[4];
+    double S[4];
+    std::vector<double> block, usig;  // 49x49 row-major
+};
+
+inline FilterOperators precompute_filter_operators(const dc_config& cfg, double r_hu = 1.0,
+                                                   double r_hv = 1.0) {
+    FilterOperators f;
+    throw_status(dc_precompute_S(&cfg, r_hu, r_hv, f.hqht, f.S), "precompute_S failed");
+    f.block.resize(49 * 49);
+    f.usig.resize(49 * 49);
+    throw_status(dc_precompute_local_svd(&cfg, f.S, f.block.data(), f.usig.data()),
+                 "precompute_local_svd failed");
+    return f;
+}
+
+/// An ensemble of particles resident on one GPU: the batched counterpart of
+/// std::vector<OceanState> + Stepper + NoiseStream per particle.
+class Ensemble {
+public:
+    Ensemble(const dc_config& cfg, int n_members, std::int64_t member_base = 0, int device = 0,
+             void* stream = nullptr)
+        : cfg_(cfg), n_(n_members) {
+        dc_status st = dc_create(&cfg, n_members, member_base, device, stream, &ctx_);
+        if (st) throw_status(st, "dc_create failed");
+    }
+    ~Ensemble() {
+        if (ctx_) dc_destroy(ctx_);
+    }
+    Ensemble(const Ensemble&) = delete;
+    Ensemble& operator=(const Ensemble&) = delete;
+    Ensemble(Ensemble&& o) noexcept : cfg_(o.cfg_), n_(o.n_), ctx_(o.ctx_) { o.ctx_ = nullptr; }
+
+    int size() const { return n_; }
+    const dc_config& config() const { return cfg_; }
+    dc_ctx* handle() { return ctx_; }
+
+    // init_double_jet (swe.hpp:459-500) broadcast to every particle
+    void init_double_jet() { check(dc_init_double_jet(ctx_)); }
+    // Stepper::model_step (swe.hpp:244-259) on every particle, n times
+    void model_step(int n = 1) { check(dc_step(ctx_, n)); }
+    // perturb_state (stochastic.hpp:164-173), counter-based noise
+    void perturb_state() { check(dc_perturb(ctx_, DC_NOISE_PHILOX, nullptr, nullptr)); }
+    // perturb_state with injected offsets [n][2] and xi [n][nxc*nyc]
+    void perturb_state(const std::int32_t* offsets, const double* xi) {
+        check(dc_perturb(ctx_, DC_NOISE_INJECTED, offsets, xi));
+    }
+    // advect_drifters
+    void set_drifters(const std::vector<double>& pos_xy, int n_drifters) {
+        check(dc_drifters_set(ctx_, pos_xy.data(), n_drifters));
+    }
+    void advect_drifters(double dt) { check(dc_drifters_advect(ctx_, dt)); }
+    // iewpf_assimilate, single-context (no collective)
+    void iewpf_assimilate(const std::vector<dc_obs>& obs, const FilterOperators& f,
+                          std::uint64_t cycle) {
+        check(dc_iewpf_assimilate(ctx_, obs.data(), static_cast<int>(obs.size()), f.S,
+                                  f.usig.data(), cycle));
+    }
+    // one DA cycle
+    void da_cycle(int n_steps, const std::vector<dc_obs>& obs, const FilterOperators& f,
+                  std::uint64_t cycle) {
+        check(dc_da_cycle(ctx_, n_steps, obs.data(), static_cast<int>(obs.size()), f.S,
+                          f.usig.data(), cycle));
+    }
+    std::vector<dc_particle_diag> diagnostics(double* w_beta = nullptr) {
+        std::vector<dc_particle_diag> d(n_);
+        double wb[2];
+        check(dc_iewpf_diagnostics(ctx_, d.data(), w_beta ? w_beta : wb));
+        return d;
+    }
+    // OceanState of particle m, Field2D layout (field.hpp:48-50)
+    void download(int m, std::vector<float>& eta, std::vector<float>& hu, std::vector<float>& hv,
+                  double* t) {
+        const size_t n = static_cast<size_t>(cfg_.nx) * cfg_.ny;
+        eta.resize(n);
+        hu.resize(n);
+        hv.resize(n);
+        check(dc_download_member(ctx_, m, eta.data(), hu.data(), hv.data(), t));
+    }
+    void upload(int m, const float* eta, const float* hu, const float* hv, double t) {
+        check(dc_upload_member(ctx_, m, eta, hu, hv, t));
+    }
+    void sync() { check(dc_sync(ctx_)); }
+
+private:
+    void check(dc_status st) {
+        if (st) throw_status(st, dc_last_error(ctx_, nullptr, nullptr, nullptr, nullptr));
+    }
+    dc_config cfg_;
+    int n_;
+    dc_ctx* ctx_ = nullptr;
+};
+
+} // namespace gpu
+} // namespace driftcast
