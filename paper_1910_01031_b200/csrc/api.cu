@@ -42,7 +42,11 @@ struct dc_ctx {
     float* rhs = nullptr;
     unsigned long long* gmax = nullptr;
     // graph of one model step
-    cudaGraphExec_t step_exec = nullptr;
+    cudaGraphExec_t step_exec = nullptr;       // step graph that scans the CFL stats first
+    cudaGraphExec_t step_exec_fused = nullptr; // step graph relying on fused stats
+    // CFL accumulator state: 0 = reset, 1 = hold the stats of the current state
+    // (fused into the last state-changing kernel), 2 = stale
+    int stats = 2;
     bool use_graph = true;
     int64_t launches = 0;
     int last_max_sub = 8;
@@ -205,12 +209,17 @@ dc_status check_member(dc_ctx* ctx, int m) {
     return DC_OK;
 }
 
-// One model step as a graph: cfl_scan -> step_begin -> while(any active){stage1, stage2,
-// substep_end}. The while condition is set on the device by substep_end.
-dc_status build_step_graph(dc_ctx* ctx) {
+// One model step as a graph: [reset + cfl_scan] -> step_begin -> while(any active){stage1,
+// stage2, substep_end}. The while condition is set on the device by substep_end. The
+// scan is skipped when the kernel that last changed the state already reduced the CFL
+// statistics of its output (stage 2, q_half_apply).
+dc_status build_step_graph(dc_ctx* ctx, bool with_scan, cudaGraphExec_t* exec) {
     cudaStream_t s = ctx->stream;
     CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+    if (with_scan) {
+        launch_reset_stats(s, ctx->sp, ctx->ctl);
+        launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+    }
     launch_step_begin(s, ctx->sp, ctx->ctl);
     cudaStreamCaptureStatus st;
     cudaGraph_t cap = nullptr;
@@ -241,18 +250,22 @@ dc_status build_step_graph(dc_ctx* ctx) {
     CU(cudaStreamDestroy(bs));
     cudaGraph_t g = nullptr;
     CU(cudaStreamEndCapture(s, &g));
-    CU(cudaGraphInstantiate(&ctx->step_exec, g, 0));
+    CU(cudaGraphInstantiate(exec, g, 0));
     CU(cudaGraphDestroy(g));
     return DC_OK;
 }
 
 // Host-driven fallback (DC_NO_GRAPH=1): guess the substep count from the previous step,
 // then confirm on the host and continue one substep at a time.
-dc_status step_host_loop(dc_ctx* ctx) {
+dc_status step_host_loop(dc_ctx* ctx, bool with_scan) {
     cudaStream_t s = ctx->stream;
-    launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+    if (with_scan) {
+        launch_reset_stats(s, ctx->sp, ctx->ctl);
+        launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+        ctx->launches += 2;
+    }
     launch_step_begin(s, ctx->sp, ctx->ctl);
-    ctx->launches += 2;
+    ctx->launches += 1;
     int done = 0;
     int guess = ctx->last_max_sub;
     while (true) {
@@ -275,6 +288,19 @@ dc_status step_host_loop(dc_ctx* ctx) {
     count_iters_kernel<<<1, 1024, 0, s>>>(ctx->ctl.sub, ctx->M, ctx->host_iters);
     ctx->launches += 1;
     return DC_OK;
+}
+
+// q_half_apply on ctx->corr with the CFL statistics of the result fused in (the
+// accumulators are reset first unless they already are).
+void apply_q_half_with_stats(dc_ctx* ctx, const int* offsets, double scale) {
+    if (ctx->stats != 0) {
+        launch_reset_stats(ctx->stream, ctx->sp, ctx->ctl);
+        ctx->launches += 1;
+    }
+    launch_q_half_apply(ctx->stream, ctx->sp, ctx->ep, ctx->corr, offsets, scale, ctx->f[0],
+                        ctx->f[1], ctx->f[2], ctx->ctl.err, ctx->ctl.err_pos, ctx->M,
+                        ctx->ctl.mx);
+    ctx->stats = 1;
 }
 
 } // namespace
@@ -409,6 +435,7 @@ dc_status dc_destroy(dc_ctx* ctx) {
     if (!ctx) return DC_OK;
     cudaStreamSynchronize(ctx->stream);
     if (ctx->step_exec) cudaGraphExecDestroy(ctx->step_exec);
+    if (ctx->step_exec_fused) cudaGraphExecDestroy(ctx->step_exec_fused);
     for (auto* q : ctx->f) cudaFree(q);
     cudaFree(ctx->ctl_mem);
     cudaFree(ctx->substep_iters);
@@ -448,6 +475,7 @@ dc_status dc_upload_member(dc_ctx* ctx, int32_t m, const float* eta, const float
                              cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyAsync(ctx->ctl.t + m, &t, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream)); // t is a stack value
+    ctx->stats = 2;
     return DC_OK;
 }
 
@@ -462,6 +490,7 @@ dc_status dc_upload_all(dc_ctx* ctx, const float* eta, const float* hu, const fl
     if (t)
         CU(cudaMemcpyAsync(ctx->ctl.t, t, ctx->M * sizeof(double), cudaMemcpyHostToDevice,
                            ctx->stream));
+    ctx->stats = 2;
     return DC_OK;
 }
 
@@ -536,13 +565,15 @@ dc_status dc_init_double_jet(dc_ctx* ctx) {
     }
     CU(cudaMemsetAsync(ctx->ctl.t, 0, ctx->M * sizeof(double), ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
+    ctx->stats = 2;
     return DC_OK;
 }
 
 dc_status dc_step(dc_ctx* ctx, int32_t n_steps) {
     if (n_steps < 0) return set_err(ctx, DC_EINVAL, "dc_step: n_steps < 0");
     if (ctx->use_graph && !ctx->step_exec) {
-        dc_status st = build_step_graph(ctx);
+        dc_status st = build_step_graph(ctx, true, &ctx->step_exec);
+        if (!st) st = build_step_graph(ctx, false, &ctx->step_exec_fused);
         if (st) {
             cudaGetLastError();
             std::fprintf(stderr, "dc_step: graph path unavailable (%s); using host loop\n",
@@ -558,15 +589,17 @@ dc_status dc_step(dc_ctx* ctx, int32_t n_steps) {
         }
     }
     for (int i = 0; i < n_steps; ++i) {
+        const bool scan = ctx->stats != 1;
         if (ctx->use_graph) {
-            CU(cudaGraphLaunch(ctx->step_exec, ctx->stream));
+            CU(cudaGraphLaunch(scan ? ctx->step_exec : ctx->step_exec_fused, ctx->stream));
             dcg::count_iters_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->ctl.sub, ctx->M,
                                                                 ctx->substep_iters);
-            ctx->launches += 3;  // cfl_scan, step_begin, count_iters (+3 per iteration)
+            ctx->launches += (scan ? 3 : 1) + 1;  // [reset, cfl_scan,] step_begin, count_iters
         } else {
-            dc_status st = step_host_loop(ctx);
+            dc_status st = step_host_loop(ctx, scan);
             if (st) return st;
         }
+        ctx->stats = 0;  // every member's final substep_end resets the accumulators
     }
     CU(cudaGetLastError());
     return DC_OK;
@@ -666,8 +699,7 @@ dc_status dc_perturb(dc_ctx* ctx, int32_t mode, const int32_t* offsets, const do
         return set_err(ctx, DC_EINVAL, "dc_perturb: unknown noise mode");
     }
     launch_coarse_soar(ctx->stream, ctx->ep, M, ctx->xi, ctx->corr, ctx->ctl.err);
-    launch_q_half_apply(ctx->stream, ctx->sp, ctx->ep, ctx->corr, ctx->offs, 1.0, ctx->f[0],
-                        ctx->f[1], ctx->f[2], ctx->ctl.err, ctx->ctl.err_pos, M);
+    apply_q_half_with_stats(ctx, ctx->offs, 1.0);
     ctx->launches += (mode == DC_NOISE_PHILOX) ? 3 : 2;
     CU(cudaGetLastError());
     return DC_OK;
@@ -683,8 +715,7 @@ dc_status dc_add_q_half(dc_ctx* ctx, const int32_t* offsets, const double* coars
                        cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     launch_coarse_soar(ctx->stream, ctx->ep, M, ctx->xi, ctx->corr, ctx->ctl.err);
-    launch_q_half_apply(ctx->stream, ctx->sp, ctx->ep, ctx->corr, ctx->offs, scale, ctx->f[0],
-                        ctx->f[1], ctx->f[2], ctx->ctl.err, ctx->ctl.err_pos, M);
+    apply_q_half_with_stats(ctx, ctx->offs, scale);
     ctx->launches += 2;
     CU(cudaGetLastError());
     return DC_OK;
@@ -730,7 +761,9 @@ dc_status dc_time_stages(dc_ctx* ctx, int32_t n_substeps, double* ms_out) {
     cudaStream_t s = ctx->stream;
     cudaEvent_t ev[3];
     for (auto& e : ev) CU(cudaEventCreate(&e));
+    launch_reset_stats(s, ctx->sp, ctx->ctl);
     launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+    ctx->stats = 2;
     launch_step_begin(s, ctx->sp, ctx->ctl);
     double t1 = 0.0, t2 = 0.0;
     for (int i = 0; i < n_substeps; ++i) {

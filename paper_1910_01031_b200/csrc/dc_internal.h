@@ -66,12 +66,14 @@ void launch_coarse_soar(cudaStream_t s, const ErrParams& ep, int M, const double
                         double* out, const int* err);
 void launch_q_half_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
                          const double* corr, const int* offsets, double scale, float* eta,
-                         float* hu, float* hv, int* err, int* err_pos, int M);
+                         float* hu, float* hv, int* err, int* err_pos, int M,
+                         unsigned* mx = nullptr);
 
 // swe.cu launchers
 void launch_cfl_scan(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
                      const float* hv, StepCtl ctl);
 void launch_step_begin(cudaStream_t s, const SweParams& sp, StepCtl ctl);
+void launch_reset_stats(cudaStream_t s, const SweParams& sp, StepCtl ctl);
 void launch_stage(cudaStream_t s, const SweParams& sp, bool exact, int stage, const float* ie,
                   const float* iu, const float* iv, const float* s0e, const float* s0u,
                   const float* s0v, float* oe, float* ou, float* ov, StepCtl ctl);

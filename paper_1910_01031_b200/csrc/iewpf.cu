@@ -24,6 +24,7 @@
 #include "dc_internal.h"
 #include "detmath.cuh"
 #include "iewpf_kernels.h"
+#include "interp_tile.cuh"
 
 namespace dcg {
 
@@ -33,8 +34,8 @@ using det::wrap1;
 using det::wrapf;
 using det::wrapi;
 
-constexpr int TX = 32, TY = 16;
-constexpr int NBMAX = TY + 2 + 3;
+using tile::TX;
+using tile::TY;
 constexpr int WIN = 11;   // pull window: coarse offsets -5..5
 constexpr int WH = 5;
 
@@ -172,30 +173,25 @@ __global__ void tile_lists_kernel(SweParams sp, ErrParams ep, const int* __restr
     counts[t] = n;
 }
 
-__device__ __forceinline__ void row_coords(const ErrParams& ep, int kk, int ok, int* b0,
-                                           double* ty) {
-    const double yc = static_cast<double>(kk - ok) * ep.inv_c;
-    *b0 = static_cast<int>(floor(yc));
-    *ty = yc - *b0;
-}
-
 // Sequential-equivalent gather of every covering observation's pull into one tile of one
 // particle (optimal_proposal_pull, SPEC.md:455-463 + add_q_half, stochastic.hpp:144-160).
+constexpr int WP = 16;  // padded window pitch: indices 11..15 read exact zeros
+
 __global__ void __launch_bounds__(256)
 pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win,
                   const int* __restrict__ cells, int n_obs, const int* __restrict__ lists,
                   const int* __restrict__ counts, int tiles_x, float* eta, float* hu, float* hv,
                   int* err, int* err_pos) {
-    __shared__ double W[WIN * WIN];
-    __shared__ double X[NBMAX][TX + 2];
-    __shared__ double D[TY + 2][TX + 2];
+    __shared__ double W[WP * WP];
+    __shared__ double X[tile::NBMAX][tile::XW];
+    __shared__ double D[tile::TY + 2][tile::XW];
     const int m = blockIdx.y;
     if (err[m]) return;
-    const int tile = blockIdx.x;
-    const int cnt = counts[tile];
+    const int tl = blockIdx.x;
+    const int cnt = counts[tl];
     if (cnt == 0) return;
-    const int j0 = (tile % tiles_x) * TX, k0 = (tile / tiles_x) * TY;
-    const int tid = threadIdx.x;
+    const int j0 = (tl % tiles_x) * tile::TX, k0 = (tl / tiles_x) * tile::TY;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
     // the tile's cells live in registers across all observations (2 per thread)
     float e[2], u[2], v[2];
@@ -203,8 +199,7 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win,
     size_t off[2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-        const int i = tid + q * 256;
-        const int k = k0 + i / TX, j = j0 + i % TX;
+        const int k = k0 + ty + 8 * q, j = j0 + tx;
         valid[q] = (k < sp.ny) && (j < sp.nx);
         off[q] = mbase + static_cast<size_t>(valid[q] ? k : 0) * sp.pitch + (valid[q] ? j : 0);
         e[q] = valid[q] ? eta[off[q]] : 0.0f;
@@ -214,66 +209,42 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win,
     bool dry = false;
     int dry_at = 0x7fffffff;
     for (int li = 0; li < cnt; ++li) {
-        const int o = lists[static_cast<size_t>(tile) * n_obs + li];
+        const int o = lists[static_cast<size_t>(tl) * n_obs + li];
         const int jo = cells[2 * o], ko = cells[2 * o + 1];
         const int oj = jo % ep.c, ok = ko % ep.c;           // align_coarse_offset
         const int ao = wrapi((jo - oj) / ep.c, ep.nxc);     // coarse_point_of
         const int bo = wrapi((ko - ok) / ep.c, ep.nyc);
         const double* wsrc = win + (static_cast<size_t>(m) * n_obs + o) * (WIN * WIN);
-        __syncthreads();  // previous obs done with W/X/D
-        for (int i = tid; i < WIN * WIN; i += 256) W[i] = wsrc[i];
-        int bfirst, blast;
-        double tdum;
-        row_coords(ep, wrap1(k0 - 1, sp.ny), ok, &bfirst, &tdum);
-        row_coords(ep, wrap1(k0 + TY, sp.ny), ok, &blast, &tdum);
-        const bool whole = ep.nyc <= NBMAX;
-        const int bstart = whole ? 0 : wrapf(bfirst - 1, ep.nyc);
-        const int nb = whole ? ep.nyc : wrapf(blast - bfirst, ep.nyc) + 4;
-        __syncthreads();
-        // coarse value of the window (zero outside): corr(a, b)
-        auto corr = [&](int a, int b) -> double {
-            const int da = wrapf(a - ao + WH, ep.nxc), db = wrapf(b - bo + WH, ep.nyc);
-            return (da < WIN && db < WIN) ? W[db * WIN + da] : 0.0;
-        };
-        for (int i = tid; i < nb * (TX + 2); i += 256) {
-            const int s = i / (TX + 2), jl = i % (TX + 2);
-            const int b = whole ? s : wrap1(bstart + s, ep.nyc);
-            const int jw = wrap1(j0 - 1 + jl, sp.nx);
-            const double xc = static_cast<double>(jw - oj) * ep.inv_c;
-            const int a0 = static_cast<int>(floor(xc));
-            const double tx = xc - a0;
-            X[s][jl] = det::catmull(corr(wrapf(a0 - 1, ep.nxc), b), corr(wrapf(a0, ep.nxc), b),
-                                    corr(wrapf(a0 + 1, ep.nxc), b), corr(wrapf(a0 + 2, ep.nxc), b),
-                                    tx);
+        __syncthreads();  // the previous observation is done with W / X / D
+        {
+            const int da = tid % WP, db = tid / WP;  // 256 threads fill the 16x16 pad
+            W[tid] = (da < WIN && db < WIN) ? wsrc[db * WIN + da] : 0.0;
         }
         __syncthreads();
-        for (int i = tid; i < (TY + 2) * (TX + 2); i += 256) {
-            const int r = i / (TX + 2), jl = i % (TX + 2);
-            const int kk = wrap1(k0 - 1 + r, sp.ny);
-            int b0;
-            double ty;
-            row_coords(ep, kk, ok, &b0, &ty);
-            int sl[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int b = wrapf(b0 - 1 + q, ep.nyc);
-                sl[q] = whole ? b : wrapf(b - bstart, ep.nyc);
-            }
-            D[r][jl] = det::catmull(X[sl[0]][jl], X[sl[1]][jl], X[sl[2]][jl], X[sl[3]][jl], ty);
-        }
-        __syncthreads();
+        const int nxc = ep.nxc, nyc = ep.nyc;
+        tile::interpolate<const double*>(
+            ep, sp.nx, sp.ny, j0, k0, oj, ok,
+            [&](int b) {
+                const int db = wrapf(b - bo + WH, nyc);
+                return W + (db < WIN ? db : WP - 1) * WP;
+            },
+            [&](const double* row, int a) { return row[a]; },
+            [&](int a) {
+                const int da = wrapf(a - ao + WH, nxc);
+                return da < WIN ? da : WP - 1;
+            },
+            X, D);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             if (!valid[q]) continue;
-            const int i = tid + q * 256;
-            const int r = i / TX + 1, jl = i % TX + 1;
+            const int r = ty + 8 * q + 1, jl = tx + 1;
             const double de = D[r][jl];
             const double dhu = -ep.cy * (D[r + 1][jl] - D[r - 1][jl]);
             const double dhv = ep.cx * (D[r][jl + 1] - D[r][jl - 1]);
             const double ee = static_cast<double>(e[q]) + 1.0 * de;
             if (!(ep.h_eq + ee > 0.0)) {
                 dry = true;
-                dry_at = min(dry_at, (k0 + r - 1) * sp.nx + (j0 + jl - 1));
+                dry_at = min(dry_at, (k0 + r - 1) * sp.nx + (j0 + tx));
             }
             e[q] = static_cast<float>(ee);
             u[q] = static_cast<float>(static_cast<double>(u[q]) + 1.0 * dhu);

@@ -19,6 +19,7 @@
 
 #include "dc_internal.h"
 #include "detmath.cuh"
+#include "interp_tile.cuh"
 
 namespace dcg {
 
@@ -72,94 +73,108 @@ __global__ void coarse_soar_kernel(ErrParams ep, int M, const double* __restrict
     }
 }
 
-constexpr int TX = 32, TY = 16;
-constexpr int NBMAX = TY + 2 + 3;  // coarse rows a tile can touch (c_omega = 1 worst case)
+using tile::TX;
+using tile::TY;
+using tile::XW;
 
-// Fine-row -> coarse-row bookkeeping of interpolate_bicubic (stochastic.hpp:97-102),
-// computed from the WRAPPED fine index exactly as the reference does.
-__device__ __forceinline__ void row_coords(const ErrParams& ep, int kk, int ok, int* b0, double* ty) {
-    const double yc = static_cast<double>(kk - ok) * ep.inv_c;
-    *b0 = static_cast<int>(floor(yc));
-    *ty = yc - *b0;
+__device__ __forceinline__ unsigned ordered_bits(float f) {
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-// Q^{1/2} tail + add (stochastic.hpp:144-160) for one (member, 32x16 tile).
+// Q^{1/2} tail + add (stochastic.hpp:144-160) for one (member, 32x16 tile). When mx is
+// given, also reduces the CFL statistics of the NEW state (Stepper::load,
+// swe.hpp:306-317) so the next model step needs no separate scan.
 __global__ void __launch_bounds__(256)
 q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
                     const int* __restrict__ offsets, double scale, float* eta, float* hu,
-                    float* hv, int* err, int* err_pos) {
-    __shared__ double X[NBMAX][TX + 2];
-    __shared__ double D[TY + 2][TX + 2];
+                    float* hv, int* err, int* err_pos, unsigned* mx) {
+    __shared__ double X[tile::NBMAX][XW];
+    __shared__ double D[TY + 2][XW];
+    __shared__ float red[3][8];
     const int m = blockIdx.z;
     if (err[m]) return;
     const int j0 = blockIdx.x * TX, k0 = blockIdx.y * TY;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
+    // issue the state loads first: their latency overlaps the interpolation passes
+    float e0[2], u0[2], v0[2];
+    size_t off[2];
+    bool valid[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int k = k0 + ty + 8 * q, j = j0 + tx;
+        valid[q] = (k < sp.ny) && (j < sp.nx);
+        off[q] = mbase + static_cast<size_t>(valid[q] ? k : 0) * sp.pitch + (valid[q] ? j : 0);
+        e0[q] = valid[q] ? eta[off[q]] : 0.0f;
+        u0[q] = valid[q] ? hu[off[q]] : 0.0f;
+        v0[q] = valid[q] ? hv[off[q]] : 0.0f;
+    }
     const int oj = offsets[2 * m], ok = offsets[2 * m + 1];
     const double* cf = corr + static_cast<size_t>(m) * ep.nxc * ep.nyc;
-    const int tid = threadIdx.x;
-
-    // coarse-row window of this tile
-    int bfirst, blast;
-    double tdummy;
-    row_coords(ep, wrapi(k0 - 1, sp.ny), ok, &bfirst, &tdummy);
-    row_coords(ep, wrapi(k0 + TY, sp.ny), ok, &blast, &tdummy);
-    const bool whole = ep.nyc <= NBMAX;
-    const int bstart = whole ? 0 : wrapi(bfirst - 1, ep.nyc);
-    const int nb = whole ? ep.nyc : wrapi(blast - bfirst, ep.nyc) + 4;
-
-    // pass 1: x-interpolation of the needed coarse rows at the tile's fine columns
-    for (int i = tid; i < nb * (TX + 2); i += blockDim.x) {
-        const int s = i / (TX + 2), jl = i % (TX + 2);
-        const int b = whole ? s : wrap1(bstart + s, ep.nyc);
-        const int jw = wrap1(j0 - 1 + jl, sp.nx);
-        const double xc = static_cast<double>(jw - oj) * ep.inv_c;
-        const int a0 = static_cast<int>(floor(xc));
-        const double tx = xc - a0;
-        const double* row = cf + b * ep.nxc;
-        X[s][jl] = det::catmull(__ldg(row + det::wrapf(a0 - 1, ep.nxc)), __ldg(row + det::wrapf(a0, ep.nxc)),
-                                __ldg(row + det::wrapf(a0 + 1, ep.nxc)), __ldg(row + det::wrapf(a0 + 2, ep.nxc)),
-                                tx);
-    }
-    __syncthreads();
-    // pass 2: y-interpolation -> delta eta on the tile + 1-cell halo
-    for (int i = tid; i < (TY + 2) * (TX + 2); i += blockDim.x) {
-        const int r = i / (TX + 2), jl = i % (TX + 2);
-        const int kk = wrap1(k0 - 1 + r, sp.ny);
-        int b0;
-        double ty;
-        row_coords(ep, kk, ok, &b0, &ty);
-        int sl[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int b = det::wrapf(b0 - 1 + q, ep.nyc);
-            sl[q] = whole ? b : det::wrapf(b - bstart, ep.nyc);
-        }
-        D[r][jl] = det::catmull(X[sl[0]][jl], X[sl[1]][jl], X[sl[2]][jl], X[sl[3]][jl], ty);
-    }
-    __syncthreads();
-    // pass 3: geostrophic balance (stochastic.hpp:122-139) + add in fp64, cast to float
+    const int nxc = ep.nxc;
+    tile::interpolate<const double*>(
+        ep, sp.nx, sp.ny, j0, k0, oj, ok,
+        [&](int b) { return cf + b * nxc; },
+        [&](const double* row, int a) { return __ldg(row + a); }, [](int a) { return a; }, X, D);
+    // geostrophic balance (stochastic.hpp:122-139) + add in fp64, cast to float
     bool dry = false;
     int dry_at = 0x7fffffff;
-    const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
-    for (int i = tid; i < TY * TX; i += blockDim.x) {
-        const int r = i / TX + 1, jl = i % TX + 1;
-        const int k = k0 + r - 1, j = j0 + jl - 1;
-        if (k >= sp.ny || j >= sp.nx) continue;
+    float mx_u = 0.0f, mx_v = 0.0f, mn_h = 3.402823466e+38f;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        if (!valid[q]) continue;
+        const int r = ty + 8 * q + 1, jl = tx + 1;
         const double de = D[r][jl];
         const double dhu = -ep.cy * (D[r + 1][jl] - D[r - 1][jl]);
         const double dhv = ep.cx * (D[r][jl + 1] - D[r][jl - 1]);
-        const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
-        const double e = static_cast<double>(eta[o]) + scale * de;
+        const double e = static_cast<double>(e0[q]) + scale * de;
         if (!(ep.h_eq + e > 0.0)) {
             dry = true;
-            dry_at = min(dry_at, k * sp.nx + j);
+            dry_at = min(dry_at, (k0 + r - 1) * sp.nx + (j0 + tx));
         }
-        eta[o] = static_cast<float>(e);
-        hu[o] = static_cast<float>(static_cast<double>(hu[o]) + scale * dhu);
-        hv[o] = static_cast<float>(static_cast<double>(hv[o]) + scale * dhv);
+        const float fe = static_cast<float>(e);
+        const float fu = static_cast<float>(static_cast<double>(u0[q]) + scale * dhu);
+        const float fv = static_cast<float>(static_cast<double>(v0[q]) + scale * dhv);
+        eta[off[q]] = fe;
+        hu[off[q]] = fu;
+        hv[off[q]] = fv;
+        if (mx) {  // load() statistics of the new state, IEEE float (swe.hpp:307-316)
+            const float h = __fadd_rn(sp.H, fe);
+            mn_h = fminf(mn_h, h);
+            const float inv = __frcp_rn(h);
+            const float c = __fsqrt_rn(__fmul_rn(sp.g, fmaxf(h, 0.0f)));
+            mx_u = fmaxf(mx_u, __fadd_rn(fabsf(__fmul_rn(fu, inv)), c));
+            mx_v = fmaxf(mx_v, __fadd_rn(fabsf(__fmul_rn(fv, inv)), c));
+        }
     }
     if (dry) {
         atomicCAS(err + m, 0, E_DRY_ADD);
         atomicMin(err_pos + m, dry_at);
+    }
+    if (mx) {
+        for (int o = 16; o > 0; o >>= 1) {
+            mx_u = fmaxf(mx_u, __shfl_xor_sync(0xffffffffu, mx_u, o));
+            mx_v = fmaxf(mx_v, __shfl_xor_sync(0xffffffffu, mx_v, o));
+            mn_h = fminf(mn_h, __shfl_xor_sync(0xffffffffu, mn_h, o));
+        }
+        if (tx == 0) {
+            red[0][ty] = mx_u;
+            red[1][ty] = mx_v;
+            red[2][ty] = mn_h;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float a = red[0][0], b = red[1][0], c = red[2][0];
+            for (int i = 1; i < 8; ++i) {
+                a = fmaxf(a, red[0][i]);
+                b = fmaxf(b, red[1][i]);
+                c = fminf(c, red[2][i]);
+            }
+            atomicMax(mx + 4 * m + 0, __float_as_uint(a));
+            atomicMax(mx + 4 * m + 1, __float_as_uint(b));
+            atomicMin(mx + 4 * m + 2, ordered_bits(c));
+        }
     }
 }
 
@@ -182,10 +197,10 @@ void launch_coarse_soar(cudaStream_t s, const ErrParams& ep, int M, const double
 
 void launch_q_half_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
                          const double* corr, const int* offsets, double scale, float* eta,
-                         float* hu, float* hv, int* err, int* err_pos, int M) {
+                         float* hu, float* hv, int* err, int* err_pos, int M, unsigned* mx) {
     dim3 grid((sp.nx + TX - 1) / TX, (sp.ny + TY - 1) / TY, M);
     q_half_apply_kernel<<<grid, 256, 0, s>>>(sp, ep, corr, offsets, scale, eta, hu, hv, err,
-                                             err_pos);
+                                             err_pos, mx);
 }
 
 } // namespace dcg
