@@ -176,75 +176,72 @@ __global__ void tile_lists_kernel(SweParams sp, ErrParams ep, const int* __restr
 // Sequential-equivalent gather of every covering observation's pull into one tile of one
 // particle (optimal_proposal_pull, SPEC.md:455-463 + add_q_half, stochastic.hpp:144-160).
 constexpr int WP = 16;  // padded window pitch: indices 11..15 read exact zeros
+constexpr int kRowsPerThread = (TY + 7) / 8;
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(tile::NT, 3)
 pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win,
                   const int* __restrict__ cells, int n_obs, const int* __restrict__ lists,
                   const int* __restrict__ counts, int tiles_x, float* eta, float* hu, float* hv,
                   int* err, int* err_pos) {
     __shared__ double W[WP * WP];
-    __shared__ double X[tile::NBMAX][tile::XW];
-    __shared__ double D[tile::TY + 2][tile::XW];
+    __shared__ tile::Smem S;
     const int m = blockIdx.y;
     if (err[m]) return;
     const int tl = blockIdx.x;
     const int cnt = counts[tl];
     if (cnt == 0) return;
-    const int j0 = (tl % tiles_x) * tile::TX, k0 = (tl / tiles_x) * tile::TY;
+    const int j0 = (tl % tiles_x) * TX, k0 = (tl / tiles_x) * TY;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
-    // the tile's cells live in registers across all observations (2 per thread)
-    float e[2], u[2], v[2];
-    bool valid[2];
-    size_t off[2];
+    // the tile's cells live in registers across all observations
+    float e[kRowsPerThread], u[kRowsPerThread], v[kRowsPerThread];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const int k = k0 + ty + 8 * q, j = j0 + tx;
-        valid[q] = (k < sp.ny) && (j < sp.nx);
-        off[q] = mbase + static_cast<size_t>(valid[q] ? k : 0) * sp.pitch + (valid[q] ? j : 0);
-        e[q] = valid[q] ? eta[off[q]] : 0.0f;
-        u[q] = valid[q] ? hu[off[q]] : 0.0f;
-        v[q] = valid[q] ? hv[off[q]] : 0.0f;
+    for (int q = 0; q < kRowsPerThread; ++q) {
+        const int r = ty + 8 * q, k = k0 + r, j = j0 + tx;
+        const bool okc = (r < TY) && (k < sp.ny) && (j < sp.nx);
+        const size_t o = mbase + static_cast<size_t>(okc ? k : 0) * sp.pitch + (okc ? j : 0);
+        e[q] = okc ? eta[o] : 0.0f;
+        u[q] = okc ? hu[o] : 0.0f;
+        v[q] = okc ? hv[o] : 0.0f;
     }
     bool dry = false;
     int dry_at = 0x7fffffff;
+    const int nxc = ep.nxc, nyc = ep.nyc;
     for (int li = 0; li < cnt; ++li) {
         const int o = lists[static_cast<size_t>(tl) * n_obs + li];
         const int jo = cells[2 * o], ko = cells[2 * o + 1];
         const int oj = jo % ep.c, ok = ko % ep.c;           // align_coarse_offset
-        const int ao = wrapi((jo - oj) / ep.c, ep.nxc);     // coarse_point_of
-        const int bo = wrapi((ko - ok) / ep.c, ep.nyc);
+        const int ao = wrapi((jo - oj) / ep.c, nxc);        // coarse_point_of
+        const int bo = wrapi((ko - ok) / ep.c, nyc);
         const double* wsrc = win + (static_cast<size_t>(m) * n_obs + o) * (WIN * WIN);
-        __syncthreads();  // the previous observation is done with W / X / D
+        __syncthreads();  // the previous observation is done with W and the tables
         {
             const int da = tid % WP, db = tid / WP;  // 256 threads fill the 16x16 pad
             W[tid] = (da < WIN && db < WIN) ? wsrc[db * WIN + da] : 0.0;
         }
-        __syncthreads();
-        const int nxc = ep.nxc, nyc = ep.nyc;
-        tile::interpolate<const double*>(
-            ep, sp.nx, sp.ny, j0, k0, oj, ok,
-            [&](int b) {
-                const int db = wrapf(b - bo + WH, nyc);
-                return W + (db < WIN ? db : WP - 1) * WP;
-            },
-            [&](const double* row, int a) { return row[a]; },
+        tile::setup(
+            S, ep, sp.nx, sp.ny, j0, k0, oj, ok,
             [&](int a) {
                 const int da = wrapf(a - ao + WH, nxc);
                 return da < WIN ? da : WP - 1;
             },
-            X, D);
+            [&](int b) {
+                const int db = wrapf(b - bo + WH, nyc);
+                return (db < WIN ? db : WP - 1) * WP;
+            });
+        tile::interpolate(S, [&](int brow, int a) { return W[brow + a]; });
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            if (!valid[q]) continue;
-            const int r = ty + 8 * q + 1, jl = tx + 1;
-            const double de = D[r][jl];
-            const double dhu = -ep.cy * (D[r + 1][jl] - D[r - 1][jl]);
-            const double dhv = ep.cx * (D[r][jl + 1] - D[r][jl - 1]);
+        for (int q = 0; q < kRowsPerThread; ++q) {
+            const int r = ty + 8 * q, k = k0 + r, j = j0 + tx;
+            if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
+            const int rr = r + 1, jl = tx + 1;
+            const double de = S.D[rr][jl];
+            const double dhu = -ep.cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
+            const double dhv = ep.cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
             const double ee = static_cast<double>(e[q]) + 1.0 * de;
             if (!(ep.h_eq + ee > 0.0)) {
                 dry = true;
-                dry_at = min(dry_at, (k0 + r - 1) * sp.nx + (j0 + tx));
+                dry_at = min(dry_at, k * sp.nx + j);
             }
             e[q] = static_cast<float>(ee);
             u[q] = static_cast<float>(static_cast<double>(u[q]) + 1.0 * dhu);
@@ -252,12 +249,14 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win,
         }
     }
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-        if (valid[q]) {
-            eta[off[q]] = e[q];
-            hu[off[q]] = u[q];
-            hv[off[q]] = v[q];
-        }
+    for (int q = 0; q < kRowsPerThread; ++q) {
+        const int r = ty + 8 * q, k = k0 + r, j = j0 + tx;
+        if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
+        const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
+        eta[o] = e[q];
+        hu[o] = u[q];
+        hv[o] = v[q];
+    }
     if (dry) {
         atomicCAS(err + m, 0, E_DRY_ADD);
         atomicMin(err_pos + m, dry_at);

@@ -75,22 +75,22 @@ __global__ void coarse_soar_kernel(ErrParams ep, int M, const double* __restrict
 
 using tile::TX;
 using tile::TY;
-using tile::XW;
 
 __device__ __forceinline__ unsigned ordered_bits(float f) {
     const unsigned b = __float_as_uint(f);
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-// Q^{1/2} tail + add (stochastic.hpp:144-160) for one (member, 32x16 tile). When mx is
+// Q^{1/2} tail + add (stochastic.hpp:144-160) for one (member, 32x30 tile). When mx is
 // given, also reduces the CFL statistics of the NEW state (Stepper::load,
 // swe.hpp:306-317) so the next model step needs no separate scan.
-__global__ void __launch_bounds__(256)
+constexpr int kRowsPerThread = (TY + 7) / 8;  // 4
+
+__global__ void __launch_bounds__(tile::NT, 4)
 q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
                     const int* __restrict__ offsets, double scale, float* eta, float* hu,
                     float* hv, int* err, int* err_pos, unsigned* mx) {
-    __shared__ double X[tile::NBMAX][XW];
-    __shared__ double D[TY + 2][XW];
+    __shared__ tile::Smem S;
     __shared__ float red[3][8];
     const int m = blockIdx.z;
     if (err[m]) return;
@@ -98,47 +98,46 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
     // issue the state loads first: their latency overlaps the interpolation passes
-    float e0[2], u0[2], v0[2];
-    size_t off[2];
-    bool valid[2];
+    float e0[kRowsPerThread], u0[kRowsPerThread], v0[kRowsPerThread];
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const int k = k0 + ty + 8 * q, j = j0 + tx;
-        valid[q] = (k < sp.ny) && (j < sp.nx);
-        off[q] = mbase + static_cast<size_t>(valid[q] ? k : 0) * sp.pitch + (valid[q] ? j : 0);
-        e0[q] = valid[q] ? eta[off[q]] : 0.0f;
-        u0[q] = valid[q] ? hu[off[q]] : 0.0f;
-        v0[q] = valid[q] ? hv[off[q]] : 0.0f;
+    for (int q = 0; q < kRowsPerThread; ++q) {
+        const int r = ty + 8 * q, k = k0 + r, j = j0 + tx;
+        const bool ok = (r < TY) && (k < sp.ny) && (j < sp.nx);
+        const size_t o = mbase + static_cast<size_t>(ok ? k : 0) * sp.pitch + (ok ? j : 0);
+        e0[q] = ok ? eta[o] : 0.0f;
+        u0[q] = ok ? hu[o] : 0.0f;
+        v0[q] = ok ? hv[o] : 0.0f;
     }
     const int oj = offsets[2 * m], ok = offsets[2 * m + 1];
     const double* cf = corr + static_cast<size_t>(m) * ep.nxc * ep.nyc;
     const int nxc = ep.nxc;
-    tile::interpolate<const double*>(
-        ep, sp.nx, sp.ny, j0, k0, oj, ok,
-        [&](int b) { return cf + b * nxc; },
-        [&](const double* row, int a) { return __ldg(row + a); }, [](int a) { return a; }, X, D);
+    tile::setup(S, ep, sp.nx, sp.ny, j0, k0, oj, ok, [](int a) { return a; },
+                [&](int b) { return b * nxc; });
+    tile::interpolate(S, [&](int brow, int a) { return __ldg(cf + brow + a); });
     // geostrophic balance (stochastic.hpp:122-139) + add in fp64, cast to float
     bool dry = false;
     int dry_at = 0x7fffffff;
     float mx_u = 0.0f, mx_v = 0.0f, mn_h = 3.402823466e+38f;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        if (!valid[q]) continue;
-        const int r = ty + 8 * q + 1, jl = tx + 1;
-        const double de = D[r][jl];
-        const double dhu = -ep.cy * (D[r + 1][jl] - D[r - 1][jl]);
-        const double dhv = ep.cx * (D[r][jl + 1] - D[r][jl - 1]);
+    for (int q = 0; q < kRowsPerThread; ++q) {
+        const int r = ty + 8 * q, k = k0 + r, j = j0 + tx;
+        if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
+        const int rr = r + 1, jl = tx + 1;
+        const double de = S.D[rr][jl];
+        const double dhu = -ep.cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
+        const double dhv = ep.cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
         const double e = static_cast<double>(e0[q]) + scale * de;
         if (!(ep.h_eq + e > 0.0)) {
             dry = true;
-            dry_at = min(dry_at, (k0 + r - 1) * sp.nx + (j0 + tx));
+            dry_at = min(dry_at, k * sp.nx + j);
         }
         const float fe = static_cast<float>(e);
         const float fu = static_cast<float>(static_cast<double>(u0[q]) + scale * dhu);
         const float fv = static_cast<float>(static_cast<double>(v0[q]) + scale * dhv);
-        eta[off[q]] = fe;
-        hu[off[q]] = fu;
-        hv[off[q]] = fv;
+        const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
+        eta[o] = fe;
+        hu[o] = fu;
+        hv[o] = fv;
         if (mx) {  // load() statistics of the new state, IEEE float (swe.hpp:307-316)
             const float h = __fadd_rn(sp.H, fe);
             mn_h = fminf(mn_h, h);
