@@ -370,8 +370,34 @@ dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base
     return st;
 }
 
+// Strip height of the SWE stage grid: balance the y-halo overhead (~0.45 rows of extra
+// work per strip-row) against the wave quantisation of
+// (x tiles x members x strips) CTAs over SMs x 3 resident CTAs.
+static void choose_strips(SweParams& P, int sms) {
+    const int xt = (P.nx + 251) / 252;
+    const double slots = static_cast<double>(sms) * 3.0;
+    double best = 1e30;
+    for (int s = std::max(1, (P.ny + 63) / 64); s <= std::max(1, (P.ny + 7) / 8); ++s) {
+        const int by = (P.ny + s - 1) / s;
+        const int strips = (P.ny + by - 1) / by;
+        const double n = static_cast<double>(xt) * P.M * strips;
+        const double waves = n / slots;
+        const double cost = std::ceil(waves) / waves * (1.0 + 0.45 / by);
+        if (cost < best - 1e-9) {
+            best = cost;
+            P.by = by;
+            P.strips = strips;
+        }
+    }
+}
+
 static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     CU(cudaSetDevice(device));
+    {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        choose_strips(ctx->sp, sms);
+    }
     if (stream) {
         ctx->stream = static_cast<cudaStream_t>(stream);
     } else {
