@@ -155,6 +155,17 @@ class ClockSampler:
                 "power_w_max": float(max(power)) if power else None}
 
 
+def reduce_max_sum(dist, backend, local, tmax, total):
+    """max over ranks of a time, sum over ranks of a count."""
+    import torch
+    dev = f"cuda:{local}" if backend == "nccl" else "cpu"
+    a = torch.tensor([tmax], dtype=torch.float64, device=dev)
+    b = torch.tensor([total], dtype=torch.float64, device=dev)
+    dist.all_reduce(a, op=dist.ReduceOp.MAX)
+    dist.all_reduce(b, op=dist.ReduceOp.SUM)
+    return float(a.item()), float(b.item())
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -274,11 +285,20 @@ def main():
     import torch
     import paper_1910_01031_b200 as pkg
 
+    # DC_BENCH_DEVICE / DC_BENCH_BACKEND=gloo exist only to exercise the multi-rank logic
+    # on a single-GPU box (ranks share the device, the all-gather is staged via the host);
+    # the product path is one GPU per rank over NCCL.
+    if os.environ.get("DC_BENCH_DEVICE") is not None:
+        local = int(os.environ["DC_BENCH_DEVICE"])
+    backend = os.environ.get("DC_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     stream = torch.cuda.Stream()
     cfg = pkg.Config(nx=args.nx, ny=args.ny, exact_fp=not args.fast)
     M = args.members
@@ -302,7 +322,13 @@ def main():
             else:
                 ens.da_cycle(5, np.zeros((0, 4)), S, usig, c)  # forecast + drifters only
                 ens.iewpf_begin(obs, S, usig, c, total, cz_ptr=cz_local.data_ptr())
-                dist.all_gather_into_tensor(cz_all, cz_local)
+                if backend == "nccl":
+                    dist.all_gather_into_tensor(cz_all, cz_local)
+                else:  # host-staged test path
+                    host = cz_local.cpu()
+                    parts = [torch.zeros_like(host) for _ in range(world)]
+                    dist.all_gather(parts, host)
+                    cz_all.copy_(torch.cat(parts))
                 ens.iewpf_finish(cz_ptr=cz_all.data_ptr())
 
         clk = ClockSampler(local)
@@ -332,12 +358,7 @@ def main():
         ens.sync()
         cell_updates = (cs1 - cs0) * cfg.nx * cfg.ny
         if dist:
-            t = torch.tensor([ms, float(cell_updates)], dtype=torch.float64, device=f"cuda:{local}")
-            tmax = t.clone()
-            dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-            dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-            ms = float(tmax[0])
-            cell_updates = float(t[1])
+            ms, cell_updates = reduce_max_sum(dist, backend, local, ms, float(cell_updates))
         value = cell_updates / (ms / 1e3)
 
         # ---- end to end through the C ABI with host buffers ----
@@ -356,11 +377,7 @@ def main():
         wall = time.perf_counter() - t0
         e2e_cu = (ens.counters()[1] - e2e_cu0) * cfg.nx * cfg.ny
         if dist:
-            t = torch.tensor([wall, float(e2e_cu)], dtype=torch.float64, device=f"cuda:{local}")
-            tmax = t.clone()
-            dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-            dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-            wall, e2e_cu = float(tmax[0]), float(t[1])
+            wall, e2e_cu = reduce_max_sum(dist, backend, local, wall, float(e2e_cu))
         e2e_value = e2e_cu / wall
         clocks = clk.stop()  # sampled from warm-up through the timed and e2e regions
 
