@@ -135,6 +135,7 @@ void derive_params(dc_ctx* c) {
     P.model_dt = g.model_dt;
     P.h_eq = g.h_eq;
     P.gd = g.g;
+    P.neg_zero = -0.0f;
     ErrParams& E = c->ep;
     E.c = g.c_omega;
     E.nxc = g.nx / g.c_omega;
@@ -375,7 +376,7 @@ dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base
 // (x tiles x members x strips) CTAs over SMs x 3 resident CTAs.
 static void choose_strips(SweParams& P, int sms) {
     const int xt = (P.nx + 251) / 252;
-    const double slots = static_cast<double>(sms) * 4.0;  // DC_SWE_MIN_BLOCKS
+    const double slots = static_cast<double>(sms) * 3.0;  // DC_SWE_MIN_BLOCKS
     double best = 1e30;
     for (int s = std::max(1, (P.ny + 63) / 64); s <= std::max(1, (P.ny + 7) / 8); ++s) {
         const int by = (P.ny + s - 1) / s;

@@ -31,6 +31,7 @@ struct SweParams {
     int by, strips;       // rows per CTA strip, strips per member
     float H, g, theta, cf_x, cf_y, inv_g, idx, idy, fH;
     double dx, dy, courant, model_dt, h_eq, gd;
+    float neg_zero;       // -0.0f, opaque to ptxas (packed-product addend, swe.cu)
 };
 
 // Per-member control block for the device-side CFL substep loop (swe.hpp:244-259).
