@@ -374,9 +374,9 @@ dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base
 // Strip height of the SWE stage grid: balance the y-halo overhead (~0.45 rows of extra
 // work per strip-row) against the wave quantisation of
 // (x tiles x members x strips) CTAs over SMs x 3 resident CTAs.
-static void choose_strips(SweParams& P, int sms) {
+static void choose_strips(SweParams& P, int sms, int per_sm) {
     const int xt = (P.nx + 251) / 252;
-    const double slots = static_cast<double>(sms) * 3.0;  // DC_SWE_MIN_BLOCKS
+    const double slots = static_cast<double>(sms) * per_sm;
     double best = 1e30;
     for (int s = std::max(1, (P.ny + 63) / 64); s <= std::max(1, (P.ny + 7) / 8); ++s) {
         const int by = (P.ny + s - 1) / s;
@@ -397,7 +397,7 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-        choose_strips(ctx->sp, sms);
+        choose_strips(ctx->sp, sms, swe_stage_occupancy());
     }
     if (stream) {
         ctx->stream = static_cast<cudaStream_t>(stream);

@@ -75,6 +75,7 @@ void launch_cfl_scan(cudaStream_t s, const SweParams& sp, const float* eta, cons
                      const float* hv, StepCtl ctl);
 void launch_step_begin(cudaStream_t s, const SweParams& sp, StepCtl ctl);
 void launch_reset_stats(cudaStream_t s, const SweParams& sp, StepCtl ctl);
+int swe_stage_occupancy();
 void launch_stage(cudaStream_t s, const SweParams& sp, bool exact, int stage, const float* ie,
                   const float* iu, const float* iv, const float* s0e, const float* s0u,
                   const float* s0v, float* oe, float* ou, float* ov, StepCtl ctl);
