@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdriftcast_gpu.so")
+# DC_LIB_PATH selects an alternative build of the same library (A/B timing of variants).
+LIB_PATH = os.environ.get("DC_LIB_PATH") or os.path.join(HERE, "libdriftcast_gpu.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "driftcast_gpu.h")
 
 DC_OK, DC_EINVAL, DC_EDRY, DC_ENONFINITE, DC_ERUNAWAY, DC_EALIGN, DC_ECUDA, DC_ESTATE = range(8)
