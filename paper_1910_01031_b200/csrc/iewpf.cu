@@ -163,7 +163,7 @@ __global__ void tile_lists_kernel(SweParams sp, ErrParams ep, const int* __restr
     const int tx = t % tiles_x, ty = t / tiles_x;
     const int j0 = tx * TX, j1 = min(j0 + TX, sp.nx) - 1;
     const int k0 = ty * TY, k1 = min(k0 + TY, sp.ny) - 1;
-    const int r = 8 * ep.c + 1;  // footprint radius, generous
+    const int r = 7 * ep.c + 1;  // footprint radius
     int n = 0;
     for (int o = 0; o < n_obs; ++o) {
         const int jo = cells[2 * o], ko = cells[2 * o + 1];

@@ -19,6 +19,7 @@
 
 #include "dc_internal.h"
 #include "detmath.cuh"
+#include "fp32_rn.cuh"
 #include "interp_tile.cuh"
 
 namespace dcg {
@@ -96,17 +97,25 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
     if (err[m]) return;
     const int j0 = blockIdx.x * TX, k0 = blockIdx.y * TY;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
+    const int j = j0 + tx;
+    const size_t pitch = sp.pitch;
+    // this thread's cells: column j, rows k0 + ty + 8q
+    const size_t cell0 = static_cast<size_t>(m) * sp.ny * pitch + static_cast<size_t>(k0 + ty) * pitch + j;
+    const size_t step = 8 * pitch;
+    bool okq[kRowsPerThread];
+#pragma unroll
+    for (int q = 0; q < kRowsPerThread; ++q) {
+        const int r = ty + 8 * q;
+        okq[q] = (r < TY) && (k0 + r < sp.ny) && (j < sp.nx);
+    }
     // issue the state loads first: their latency overlaps the interpolation passes
     float e0[kRowsPerThread], u0[kRowsPerThread], v0[kRowsPerThread];
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = ty + 8 * q, k = k0 + r, j = j0 + tx;
-        const bool ok = (r < TY) && (k < sp.ny) && (j < sp.nx);
-        const size_t o = mbase + static_cast<size_t>(ok ? k : 0) * sp.pitch + (ok ? j : 0);
-        e0[q] = ok ? eta[o] : 0.0f;
-        u0[q] = ok ? hu[o] : 0.0f;
-        v0[q] = ok ? hv[o] : 0.0f;
+        const size_t o = cell0 + q * step;
+        e0[q] = okq[q] ? eta[o] : 0.0f;
+        u0[q] = okq[q] ? hu[o] : 0.0f;
+        v0[q] = okq[q] ? hv[o] : 0.0f;
     }
     const int oj = offsets[2 * m], ok = offsets[2 * m + 1];
     const double* cf = corr + static_cast<size_t>(m) * ep.nxc * ep.nyc;
@@ -118,31 +127,31 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
     bool dry = false;
     int dry_at = 0x7fffffff;
     float mx_u = 0.0f, mx_v = 0.0f, mn_h = 3.402823466e+38f;
+    const double cy = ep.cy, cx = ep.cx, heq = ep.h_eq;
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = ty + 8 * q, k = k0 + r, j = j0 + tx;
-        if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
-        const int rr = r + 1, jl = tx + 1;
+        if (!okq[q]) continue;
+        const int rr = ty + 8 * q + 1, jl = tx + 1;
         const double de = S.D[rr][jl];
-        const double dhu = -ep.cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
-        const double dhv = ep.cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
+        const double dhu = -cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
+        const double dhv = cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
         const double e = static_cast<double>(e0[q]) + scale * de;
-        if (!(ep.h_eq + e > 0.0)) {
+        if (!(heq + e > 0.0)) {
             dry = true;
-            dry_at = min(dry_at, k * sp.nx + j);
+            dry_at = min(dry_at, (k0 + rr - 1) * sp.nx + j);
         }
         const float fe = static_cast<float>(e);
         const float fu = static_cast<float>(static_cast<double>(u0[q]) + scale * dhu);
         const float fv = static_cast<float>(static_cast<double>(v0[q]) + scale * dhv);
-        const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
+        const size_t o = cell0 + q * step;
         eta[o] = fe;
         hu[o] = fu;
         hv[o] = fv;
         if (mx) {  // load() statistics of the new state, IEEE float (swe.hpp:307-316)
             const float h = __fadd_rn(sp.H, fe);
             mn_h = fminf(mn_h, h);
-            const float inv = __frcp_rn(h);
-            const float c = __fsqrt_rn(__fmul_rn(sp.g, fmaxf(h, 0.0f)));
+            const float inv = rcp_rn(h);
+            const float c = sqrt_rn(__fmul_rn(sp.g, fmaxf(h, 0.0f)));
             mx_u = fmaxf(mx_u, __fadd_rn(fabsf(__fmul_rn(fu, inv)), c));
             mx_v = fmaxf(mx_v, __fadd_rn(fabsf(__fmul_rn(fv, inv)), c));
         }
