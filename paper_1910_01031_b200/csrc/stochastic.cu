@@ -77,6 +77,11 @@ __global__ void coarse_soar_kernel(ErrParams ep, int M, const double* __restrict
 using tile::TX;
 using tile::TY;
 
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
+}
+
 __device__ __forceinline__ unsigned ordered_bits(float f) {
     const unsigned b = __float_as_uint(f);
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
@@ -86,12 +91,16 @@ __device__ __forceinline__ unsigned ordered_bits(float f) {
 // given, also reduces the CFL statistics of the NEW state (Stepper::load,
 // swe.hpp:306-317) so the next model step needs no separate scan.
 constexpr int kRowsPerThread = (TY + 7) / 8;  // 4
+#ifndef DC_QHALF_MIN_BLOCKS
+#define DC_QHALF_MIN_BLOCKS 6
+#endif
 
-__global__ void __launch_bounds__(tile::NT, 4)
+__global__ void __launch_bounds__(tile::NT, DC_QHALF_MIN_BLOCKS)
 q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
                     const int* __restrict__ offsets, double scale, float* eta, float* hu,
                     float* hv, int* err, int* err_pos, unsigned* mx) {
     __shared__ tile::Smem S;
+    __shared__ float ST[3][TY][TX];
     __shared__ float red[3][8];
     const int m = blockIdx.z;
     if (err[m]) return;
@@ -108,15 +117,18 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
         const int r = ty + 8 * q;
         okq[q] = (r < TY) && (k0 + r < sp.ny) && (j < sp.nx);
     }
-    // issue the state loads first: their latency overlaps the interpolation passes
-    float e0[kRowsPerThread], u0[kRowsPerThread], v0[kRowsPerThread];
+    // stage the tile's state in shared memory with cp.async first: the loads' latency
+    // overlaps the interpolation passes without holding registers
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
+        if (!okq[q]) continue;
         const size_t o = cell0 + q * step;
-        e0[q] = okq[q] ? eta[o] : 0.0f;
-        u0[q] = okq[q] ? hu[o] : 0.0f;
-        v0[q] = okq[q] ? hv[o] : 0.0f;
+        const int r = ty + 8 * q;
+        cp_async4(&ST[0][r][tx], eta + o);
+        cp_async4(&ST[1][r][tx], hu + o);
+        cp_async4(&ST[2][r][tx], hv + o);
     }
+    asm volatile("cp.async.commit_group;\n" ::);
     const int oj = offsets[2 * m], ok = offsets[2 * m + 1];
     const double* cf = corr + static_cast<size_t>(m) * ep.nxc * ep.nyc;
     const int nxc = ep.nxc;
@@ -128,6 +140,7 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
     int dry_at = 0x7fffffff;
     float mx_u = 0.0f, mx_v = 0.0f, mn_h = 3.402823466e+38f;
     const double cy = ep.cy, cx = ep.cx, heq = ep.h_eq;
+    asm volatile("cp.async.wait_group 0;\n" ::);  // own copies only: no barrier needed
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
         if (!okq[q]) continue;
@@ -135,14 +148,15 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
         const double de = S.D[rr][jl];
         const double dhu = -cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
         const double dhv = cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
-        const double e = static_cast<double>(e0[q]) + scale * de;
+        const int r = rr - 1;
+        const double e = static_cast<double>(ST[0][r][tx]) + scale * de;
         if (!(heq + e > 0.0)) {
             dry = true;
             dry_at = min(dry_at, (k0 + rr - 1) * sp.nx + j);
         }
         const float fe = static_cast<float>(e);
-        const float fu = static_cast<float>(static_cast<double>(u0[q]) + scale * dhu);
-        const float fv = static_cast<float>(static_cast<double>(v0[q]) + scale * dhv);
+        const float fu = static_cast<float>(static_cast<double>(ST[1][r][tx]) + scale * dhu);
+        const float fv = static_cast<float>(static_cast<double>(ST[2][r][tx]) + scale * dhv);
         const size_t o = cell0 + q * step;
         eta[o] = fe;
         hu[o] = fu;
