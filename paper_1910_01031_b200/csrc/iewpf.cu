@@ -155,9 +155,11 @@ __device__ __forceinline__ bool overlaps(int lo, int hi, int t0, int t1, int n) 
     return !(t1 < a && t0 > b - n);  // [a, n-1] U [0, b-n]
 }
 
-// per fine tile: ascending ids of the observations whose pull footprint may touch it
+// per fine tile: ascending ids of the observations whose pull footprint may touch it, with
+// each observation's coarse alignment (align_coarse_offset / coarse_point_of,
+// grid.hpp:106-117) so the pull does no integer division
 __global__ void tile_lists_kernel(SweParams sp, ErrParams ep, const int* __restrict__ cells,
-                                  int n_obs, int tiles_x, int n_tiles, int* lists, int* counts) {
+                                  int n_obs, int tiles_x, int n_tiles, int4* lists, int* counts) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n_tiles) return;
     const int tx = t % tiles_x, ty = t / tiles_x;
@@ -167,8 +169,12 @@ __global__ void tile_lists_kernel(SweParams sp, ErrParams ep, const int* __restr
     int n = 0;
     for (int o = 0; o < n_obs; ++o) {
         const int jo = cells[2 * o], ko = cells[2 * o + 1];
-        if (overlaps(jo - r, jo + r, j0, j1, sp.nx) && overlaps(ko - r, ko + r, k0, k1, sp.ny))
-            lists[static_cast<size_t>(t) * n_obs + n++] = o;
+        if (overlaps(jo - r, jo + r, j0, j1, sp.nx) && overlaps(ko - r, ko + r, k0, k1, sp.ny)) {
+            const int oj = jo % ep.c, ok = ko % ep.c;
+            lists[static_cast<size_t>(t) * n_obs + n++] =
+                make_int4(o, oj | (ok << 16), wrapi((jo - oj) / ep.c, ep.nxc),
+                          wrapi((ko - ok) / ep.c, ep.nyc));
+        }
     }
     counts[t] = n;
 }
@@ -179,8 +185,8 @@ constexpr int WP = 16;  // padded window pitch: indices 11..15 read exact zeros
 constexpr int kRowsPerThread = (TY + 7) / 8;
 
 __global__ void __launch_bounds__(tile::NT, 3)
-pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win,
-                  const int* __restrict__ cells, int n_obs, const int* __restrict__ lists,
+pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, int n_obs,
+                  const int4* __restrict__ lists,
                   const int* __restrict__ counts, int tiles_x, float* eta, float* hu, float* hv,
                   int* err, int* err_pos) {
     __shared__ double W[WP * WP];
@@ -208,11 +214,9 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win,
     int dry_at = 0x7fffffff;
     const int nxc = ep.nxc, nyc = ep.nyc;
     for (int li = 0; li < cnt; ++li) {
-        const int o = lists[static_cast<size_t>(tl) * n_obs + li];
-        const int jo = cells[2 * o], ko = cells[2 * o + 1];
-        const int oj = jo % ep.c, ok = ko % ep.c;           // align_coarse_offset
-        const int ao = wrapi((jo - oj) / ep.c, nxc);        // coarse_point_of
-        const int bo = wrapi((ko - ok) / ep.c, nyc);
+        const int4 ent = lists[static_cast<size_t>(tl) * n_obs + li];
+        const int o = ent.x;
+        const int oj = ent.y & 0xffff, ok = ent.y >> 16, ao = ent.z, bo = ent.w;
         const double* wsrc = win + (static_cast<size_t>(m) * n_obs + o) * (WIN * WIN);
         __syncthreads();  // the previous observation is done with W and the tables
         {
@@ -538,7 +542,7 @@ void launch_tile_lists(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
     const int tiles_x = (sp.nx + TX - 1) / TX, tiles_y = (sp.ny + TY - 1) / TY;
     const int n_tiles = tiles_x * tiles_y;
     tile_lists_kernel<<<(n_tiles + 127) / 128, 128, 0, s>>>(sp, ep, cells, n_obs, tiles_x, n_tiles,
-                                                           lists, counts);
+                                                           reinterpret_cast<int4*>(lists), counts);
     *n_tiles_out = n_tiles;
     *tiles_x_out = tiles_x;
 }
@@ -547,7 +551,8 @@ void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
                        const int* cells, int n_obs, const int* lists, const int* counts,
                        int n_tiles, int tiles_x, float* eta, float* hu, float* hv, int* err,
                        int* err_pos, int M) {
-    pull_apply_kernel<<<dim3(n_tiles, M), 256, 0, s>>>(sp, ep, win, cells, n_obs, lists, counts,
+    pull_apply_kernel<<<dim3(n_tiles, M), 256, 0, s>>>(sp, ep, win, n_obs,
+                                                       reinterpret_cast<const int4*>(lists), counts,
                                                        tiles_x, eta, hu, hv, err, err_pos);
 }
 

@@ -14,7 +14,7 @@ struct IewpfBuffers {
     double* d = nullptr;      // [M][n_obs][2] innovations
     double* sd = nullptr;     // [M][n_obs][2] S*d
     double* win = nullptr;    // [M][n_obs][121] pull windows (SOAR(SOAR(dipole)))
-    int* tile_lists = nullptr;// [n_tiles][cap_obs] obs ids per fine tile (ascending)
+    int* tile_lists = nullptr;// [n_tiles][cap_obs] int4 {obs id, oj | ok << 16, ao, bo}, ascending id
     int* tile_count = nullptr;// [n_tiles]
     double* nu = nullptr;     // [M][nr]
     double* scal = nullptr;   // [M][8]: c, phi, gamma, zeta, alpha, xx, nn, nx
