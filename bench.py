@@ -426,8 +426,11 @@ def main():
         "dtype": "f32 state (SWE stencil) / f64 covariance + filter scalars",
         "data": "synthetic: double-jet IC, Philox model error, twin-experiment truth with "
                 f"{obs_all.shape[1]} {args.obs}, R=I",
-        "config": {"workload": "configs[1]: double-jet IEWPF, 100 members/GPU, 64 drifter obs "
-                               "every 5 min, drifter forecast copies in every member",
+        "config": {"workload": ("configs[1]: double-jet IEWPF, 100 members/GPU, 64 drifter obs "
+                                "every 5 min, drifter forecast copies in every member")
+                   if args.obs == "drifters" else
+                   ("configs[2]: double-jet IEWPF, 100 members/GPU, 240 moored-buoy obs every "
+                    "5 min, drifter forecast copies in every member"),
                    "nx": cfg.nx, "ny": cfg.ny, "members_per_gpu": M, "members_total": total,
                    "n_obs": int(obs_all.shape[1]), "obs": args.obs, "cycle": "5 x 60 s steps, "
                    "model error after 4, IEWPF analysis", "exact_fp": not args.fast,

@@ -784,28 +784,33 @@ dc_status dc_counters(dc_ctx* ctx, uint64_t* out) {
 
 dc_status dc_time_stages(dc_ctx* ctx, int32_t n_substeps, double* ms_out) {
     // One model step's worth of substeps launched individually with CUDA events around
-    // each stage kernel on the context stream (advances the state like dc_step).
+    // each stage kernel on the context stream (advances the state like dc_step). All
+    // launches and events are queued back to back and read after one synchronisation,
+    // so each interval is the kernel's duration plus the queued-launch gap.
+    if (n_substeps <= 0 || n_substeps > 64) return set_err(ctx, DC_EINVAL, "n_substeps in 1..64");
     cudaStream_t s = ctx->stream;
-    cudaEvent_t ev[3];
+    std::vector<cudaEvent_t> ev(3 * static_cast<size_t>(n_substeps));
     for (auto& e : ev) CU(cudaEventCreate(&e));
     launch_reset_stats(s, ctx->sp, ctx->ctl);
     launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
     ctx->stats = 2;
     launch_step_begin(s, ctx->sp, ctx->ctl);
-    double t1 = 0.0, t2 = 0.0;
     for (int i = 0; i < n_substeps; ++i) {
-        CU(cudaEventRecord(ev[0], s));
+        CU(cudaEventRecord(ev[3 * i], s));
         launch_stage(s, ctx->sp, ctx->exact, 1, ctx->f[0], ctx->f[1], ctx->f[2], nullptr, nullptr,
                      nullptr, ctx->f[3], ctx->f[4], ctx->f[5], ctx->ctl);
-        CU(cudaEventRecord(ev[1], s));
+        CU(cudaEventRecord(ev[3 * i + 1], s));
         launch_stage(s, ctx->sp, ctx->exact, 2, ctx->f[3], ctx->f[4], ctx->f[5], ctx->f[0],
                      ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
-        CU(cudaEventRecord(ev[2], s));
+        CU(cudaEventRecord(ev[3 * i + 2], s));
         launch_substep_end(s, ctx->sp, ctx->ctl, 0ull, 0);
-        CU(cudaEventSynchronize(ev[2]));
+    }
+    CU(cudaStreamSynchronize(s));
+    double t1 = 0.0, t2 = 0.0;
+    for (int i = 0; i < n_substeps; ++i) {
         float a = 0.f, b = 0.f;
-        CU(cudaEventElapsedTime(&a, ev[0], ev[1]));
-        CU(cudaEventElapsedTime(&b, ev[1], ev[2]));
+        CU(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
+        CU(cudaEventElapsedTime(&b, ev[3 * i + 1], ev[3 * i + 2]));
         t1 += a;
         t2 += b;
     }
