@@ -34,7 +34,9 @@ typedef enum dc_status {
     DC_ERUNAWAY = 4,   /* std::runtime_error "model_step: substep count exploded" */
     DC_EALIGN = 5,     /* apply_q_half_T: observation not co-located */
     DC_ECUDA = 6,      /* CUDA runtime failure */
-    DC_ESTATE = 7      /* API misuse (bad member index, wrong call order) */
+    DC_ESTATE = 7,     /* API misuse (bad member index, wrong call order) */
+    DC_EIO = 8,        /* std::runtime_error from snapshot / file I/O (state.hpp:71-116) */
+    DC_ECOLLAPSE = 9   /* standard PF weights: every weight underflows */
 } dc_status;
 
 /* Parameter block: ModelGrid + PhysParams + SchemeParams + ErrorParams + seed. */
@@ -131,6 +133,81 @@ dc_status dc_drifters_set(dc_ctx* ctx, const double* pos, int32_t n_d);
 dc_status dc_drifters_advect(dc_ctx* ctx, double dt);
 /* positions and winding counts [n_members][n_d][2] (synchronous). */
 dc_status dc_drifters_get(dc_ctx* ctx, double* pos, int32_t* wind);
+/* number of drifter copies per member (DC_ESTATE when none are set). */
+dc_status dc_drifters_count(dc_ctx* ctx, int32_t* n_d);
+
+/* ---- snapshots and checkpoints (state.hpp:43-116) ----------- */
+/* The context's parameters and member slice. */
+dc_status dc_get_config(dc_ctx* ctx, dc_config* cfg, int32_t* n_members, int64_t* member_base);
+/* save_snapshot (state.hpp:71-85) of member m to a file: "DCST" | u32 version 1 | u32 nx |
+ * u32 ny | f64 t | eta f32[nx*ny] | hu | hv, little endian, byte-identical to the
+ * reference writer. Synchronous. */
+dc_status dc_save_snapshot(dc_ctx* ctx, int32_t m, const char* path);
+/* load_snapshot (state.hpp:93-114) into member m, with the reference's checks and
+ * messages (bad magic, unsupported version, implausible extents, truncated stream);
+ * extents must equal the context grid (DC_EINVAL otherwise). Synchronous. */
+dc_status dc_load_snapshot(dc_ctx* ctx, int32_t m, const char* path);
+/* Checkpoint directory (SPEC.md ensemble_engine External Interfaces):
+ * dir/ensemble/particle_<i>.dcst for every member (global id i), dir/rng_state.txt (master
+ * seed, model-error draw counter, filter cycle: the whole counter-based RNG state) and
+ * dir/meta.txt (parameter echo). The directory and dir/ensemble are created if absent.
+ * Restoring reproduces the uninterrupted run bit for bit. */
+dc_status dc_checkpoint_save(dc_ctx* ctx, const char* dir, uint64_t filter_cycle);
+dc_status dc_checkpoint_load(dc_ctx* ctx, const char* dir, uint64_t* filter_cycle);
+
+/* ---- twin experiment either side of the path ------------------- */
+/* One observation record (SPEC.md ObservationRecord + file grammar). */
+typedef struct dc_obs_record {
+    double time;      /* s */
+    int32_t kind;     /* 0 drifter, 1 mooring */
+    int32_t id;       /* platform id */
+    double x, y;      /* m */
+    double y_hu, y_hv;
+} dc_obs_record;
+/* Observation noise eps ~ N(0, diag(r_hu, r_hv)) of platforms
+ * (kind, ids[i]) at observation index obs_index: counter-based Philox keyed by
+ * stream_seed(seed, obs_noise, kind << 32 | id) (rng.hpp:21,35-40), one normal pair per
+ * index. eps_out[n][2]. Synchronous. */
+dc_status dc_obs_noise(dc_ctx* ctx, int32_t kind, const int32_t* ids, int32_t n,
+                       uint64_t obs_index, double r_hu, double r_hv, double* eps_out);
+/* observe_drifter of n truth drifters: y = (dx/dt_obs * H_eq,
+ * dy/dt_obs * H_eq) + eps, displacement by the minimal periodic image; eps may be NULL.
+ * Positions [n][2] wrapped into the domain. Synchronous. */
+dc_status dc_observe_drifters(dc_ctx* ctx, const double* prev_xy, const double* cur_xy,
+                              int32_t n, double dt_obs, const double* eps, double* y_out);
+/* Standard particle-filter log-likelihood -1/2 d^T R^-1 d (R = diag(r_hu, r_hv)) of every
+ * member with the eta-compensated innovations -> loglik[n_members];
+ * failed members get -inf. Synchronous. */
+dc_status dc_pf_loglik(dc_ctx* ctx, const dc_obs* obs, int32_t n_obs, double r_hu, double r_hv,
+                       double* loglik_out);
+/* Normalised weights from n log-likelihoods (all ranks' values, global particle order);
+ * DC_ECOLLAPSE when every exp(loglik) underflows ("ensemble collapse"), with
+ * the max log-weight in *max_loglik. Host only. */
+dc_status dc_pf_weights(const double* loglik, int32_t n, double* w_out, double* max_loglik);
+/* residual_resample: floor(n w_i) copies, residual slots by multinomial
+ * draws (Philox keyed by stream_seed(seed, resample, 0), counter {slot, 0, cycle}) ->
+ * idx_out[n], ascending. Host only. */
+dc_status dc_residual_resample(const double* w, int32_t n, uint64_t seed, uint64_t cycle,
+                               int32_t* idx_out);
+/* Resampling by copy on the device: member m <- member idx[m] (fields, time, drifter
+ * copies), local indices. Synchronous. */
+dc_status dc_resample_members(dc_ctx* ctx, const int32_t* idx);
+/* forecast_error of the drifter copies against
+ * truth positions [n_d][2]: E = sqrt(mean_d E_d), E_d = mean over members of the squared
+ * minimal-image distance to truth; RMSE likewise about the ensemble mean of the unwrapped
+ * positions. Ed / Rd ([n_d]) may be NULL. Synchronous. */
+dc_status dc_forecast_error(dc_ctx* ctx, const double* truth_xy, double* E, double* RMSE,
+                            double* Ed, double* Rd);
+/* Observation file: UTF-8 lines "time,kind,id,x,y,y_hu,y_hv" with kind
+ * "drifter" | "mooring" and %.17g numbers (exact round trip). read: *n_out = records in
+ * the file; recs may be NULL to count; DC_EINVAL if capacity is too small. Host only. */
+dc_status dc_obs_file_write(const char* path, const dc_obs_record* recs, int32_t n,
+                            int32_t append);
+dc_status dc_obs_file_read(const char* path, dc_obs_record* recs, int32_t capacity,
+                           int32_t* n_out);
+/* Trajectory output: "time,particle,drifter,x,y,wind_x,wind_y" for every
+ * member's drifter copies, global particle ids. Synchronous. */
+dc_status dc_trajectory_write(dc_ctx* ctx, const char* path, double time, int32_t append);
 
 /* ---- IEWPF --------------------------------------------------- */
 /* precompute_S on the host in fp64: HQH^T and S = (HQH^T+R)^-1,

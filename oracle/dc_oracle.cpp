@@ -1274,4 +1274,162 @@ double orc_dot_tree(const double* a, const double* b, int n) {
     return dot_tree(a, b, static_cast<size_t>(n));
 }
 
+// --------------------------------------------------------------------------------------
+// §8(f): twin-experiment operators either side of the path (SPEC.md:343-401, 525-543,
+// 674-682). Same definitions as the library's; restated here.
+// --------------------------------------------------------------------------------------
+
+/// observation noise eps ~ N(0, diag(r_hu, r_hv)) of platform (kind, id) at index n:
+/// key stream_seed(seed, obs_noise, kind << 32 | id), pair 0 of draw n on substream 0
+int orc_obs_noise(const orc_params* p, int kind, const int32_t* ids, int n, uint64_t obs_index,
+                  double r_hu, double r_hv, double* eps) {
+    const double sh = std::sqrt(r_hu), sv = std::sqrt(r_hv);
+    for (int i = 0; i < n; ++i) {
+        const uint64_t platform = (static_cast<uint64_t>(static_cast<uint32_t>(kind)) << 32) |
+                                  static_cast<uint32_t>(ids[i]);
+        double z[2];
+        philox_normals(stream_key(p->seed, TAG_OBS_NOISE, platform), 0u, obs_index, 2, z);
+        eps[2 * i] = sh * z[0];
+        eps[2 * i + 1] = sv * z[1];
+    }
+    return O_OK;
+}
+
+static double min_image(double d, double len) {
+    if (d > 0.5 * len) return d - len;
+    if (d < -0.5 * len) return d + len;
+    return d;
+}
+
+/// observe_drifter: y = (dx/dt_obs * H, dy/dt_obs * H) + eps with the
+/// minimal periodic image displacement
+int orc_observe_drifters(const orc_params* p, const double* prev, const double* cur, int n,
+                         double dt_obs, const double* eps, double* y) {
+    if (!(dt_obs > 0.0)) return fail(O_EINVAL, "observe_drifter: dt_obs must be > 0");
+    const double lx = p->nx * p->dx, ly = p->ny * p->dy;
+    for (int i = 0; i < n; ++i) {
+        const double ddx = min_image(cur[2 * i] - prev[2 * i], lx);
+        const double ddy = min_image(cur[2 * i + 1] - prev[2 * i + 1], ly);
+        double a = ddx / dt_obs * p->h_eq, b = ddy / dt_obs * p->h_eq;
+        if (eps) {
+            a = a + eps[2 * i];
+            b = b + eps[2 * i + 1];
+        }
+        y[2 * i] = a;
+        y[2 * i + 1] = b;
+    }
+    return O_OK;
+}
+
+/// standard PF log-likelihood of one particle: -1/2 sum_o (d0^2/r_hu +
+/// d1^2/r_hv) in observation order, d the eta-compensated innovation
+int orc_pf_loglik(const orc_params* p, const float* eta, const float* hu, const float* hv,
+                  int n_obs, const double* obs, double r_hu, double r_hv, double* loglik) {
+    double s = 0.0;
+    for (int o = 0; o < n_obs; ++o) {
+        int j, k;
+        int rc = locate(p, obs[4 * o], obs[4 * o + 1], &j, &k);
+        if (rc) return rc;
+        double d[2];
+        innovation_at(p, eta, hu, hv, j, k, obs[4 * o + 2], obs[4 * o + 3], d);
+        s += d[0] * d[0] / r_hu + d[1] * d[1] / r_hv;
+    }
+    *loglik = -0.5 * s;
+    return O_OK;
+}
+
+/// normalisation of standard PF weights: exp(l - max) / sum, index order; returns O_EINVAL
+/// ("ensemble collapse") when every exp(l) underflows
+int orc_pf_weights(const double* loglik, int n, double* w, double* max_loglik) {
+    double mx = -std::numeric_limits<double>::infinity();
+    for (int i = 0; i < n; ++i)
+        if (loglik[i] > mx) mx = loglik[i];
+    *max_loglik = mx;
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) {
+        w[i] = std::exp(loglik[i] - mx);
+        s += w[i];
+    }
+    for (int i = 0; i < n; ++i) w[i] = w[i] / s;
+    if (mx < -745.13321910194122) return fail(O_EINVAL, "ensemble collapse");
+    return O_OK;
+}
+
+/// residual_resample: floor(n w_i + 1e-12) copies, residual slots by
+/// inverse CDF on the ascending cumulative residuals with uniforms from Philox keyed by
+/// stream_seed(seed, resample, 0), counter {slot, 0, cycle}; ascending output
+int orc_residual_resample(const double* w, int n, uint64_t seed, uint64_t cycle, int32_t* idx) {
+    std::vector<long long> cnt(n, 0);
+    std::vector<double> res(n, 0.0), cum(n, 0.0);
+    long long used = 0;
+    for (int i = 0; i < n; ++i) {
+        const double x = static_cast<double>(n) * w[i];
+        const double f = std::floor(x + 1e-12);
+        cnt[i] = static_cast<long long>(f);
+        res[i] = (x - f > 0.0) ? x - f : 0.0;
+        used += cnt[i];
+    }
+    if (used > n) return fail(O_EINVAL, "residual_resample: weights exceed 1");
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) {
+        s += res[i];
+        cum[i] = s;
+    }
+    const uint64_t key = stream_key(seed, 7, 0);
+    for (long long r = 0; r < n - used; ++r) {
+        uint32_t ctr[4] = {static_cast<uint32_t>(r), 0u, static_cast<uint32_t>(cycle),
+                           static_cast<uint32_t>(cycle >> 32)};
+        uint32_t x[4];
+        philox4x32_10(ctr, key, x);
+        const uint64_t a = ((static_cast<uint64_t>(x[0] >> 5)) << 26) | (x[1] >> 6);
+        const double u = static_cast<double>(a) * 0x1.0p-53 * s;
+        int i = 0;
+        while (i < n - 1 && !(cum[i] > u)) ++i;  // first i with cum[i] > u
+        cnt[i] += 1;
+    }
+    int k = 0;
+    for (int i = 0; i < n; ++i)
+        for (long long c = 0; c < cnt[i]; ++c) idx[k++] = i;
+    return O_OK;
+}
+
+/// forecast_error for n_d drifters over n_m members:
+/// pos/wind [m][d][2]; E_d = mean_m |x - truth|^2, RMSE_d = mean_m |x - mean|^2 (minimal
+/// images; mean of the unwrapped positions wrapped back), E = sqrt(mean_d E_d)
+int orc_forecast_error(const orc_params* p, int n_m, int n_d, const double* pos,
+                       const int32_t* wind, const double* truth, double* E, double* R,
+                       double* ed, double* rd) {
+    const double lx = p->nx * p->dx, ly = p->ny * p->dy;
+    double se_all = 0.0, sr_all = 0.0;
+    for (int d = 0; d < n_d; ++d) {
+        double se = 0.0, sx = 0.0, sy = 0.0;
+        for (int m = 0; m < n_m; ++m) {
+            const size_t q = (static_cast<size_t>(m) * n_d + d) * 2;
+            const double ex = min_image(pos[q] - truth[2 * d], lx);
+            const double ey = min_image(pos[q + 1] - truth[2 * d + 1], ly);
+            se = se + (ex * ex + ey * ey);
+            sx = sx + (pos[q] + wind[q] * lx);
+            sy = sy + (pos[q + 1] + wind[q + 1] * ly);
+        }
+        const double mx = sx / n_m, my = sy / n_m;
+        double wx = std::fmod(mx, lx), wy = std::fmod(my, ly);
+        if (wx < 0.0) wx += lx;
+        if (wy < 0.0) wy += ly;
+        double sr = 0.0;
+        for (int m = 0; m < n_m; ++m) {
+            const size_t q = (static_cast<size_t>(m) * n_d + d) * 2;
+            const double ex = min_image(pos[q] - wx, lx), ey = min_image(pos[q + 1] - wy, ly);
+            sr = sr + (ex * ex + ey * ey);
+        }
+        const double a = se / n_m, b = sr / n_m;
+        if (ed) ed[d] = a;
+        if (rd) rd[d] = b;
+        se_all += a;
+        sr_all += b;
+    }
+    *E = std::sqrt(se_all / n_d);
+    *R = std::sqrt(sr_all / n_d);
+    return O_OK;
+}
+
 } // extern "C"

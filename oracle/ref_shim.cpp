@@ -115,6 +115,28 @@ int ref_init_double_jet(const orc_params* p, float* eta, float* hu, float* hv, c
     });
 }
 
+/// save_snapshot (state.hpp:78-83) of one state to a file, the reference writer.
+int ref_save_snapshot(const orc_params* p, const float* eta, const float* hu, const float* hv,
+                      double t, const char* path, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        ModelGrid g = grid_of(p);
+        OceanState s = state_in(g, eta, hu, hv, t);
+        save_snapshot(std::string(path), s);
+    });
+}
+
+/// load_snapshot (state.hpp:110-114): fields out, *t; errors as the reference throws them.
+int ref_load_snapshot(const orc_params* p, const char* path, float* eta, float* hu, float* hv,
+                      double* t, char* err, int errlen) {
+    return guarded(err, errlen, [&] {
+        OceanState s = load_snapshot(std::string(path));
+        if (s.nx() != p->nx || s.ny() != p->ny)
+            throw std::invalid_argument("ref_load_snapshot: extents differ from the params");
+        state_out(s, eta, hu, hv);
+        *t = s.t;
+    });
+}
+
 /// n_steps calls of Stepper::model_step (swe.hpp:244-259) on one member.
 int ref_model_step(const orc_params* p, float* eta, float* hu, float* hv, double* t,
                    int n_steps, char* err, int errlen) {

@@ -14,13 +14,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DC_LIB_PATH") or os.path.join(HERE, "libdriftcast_gpu.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "driftcast_gpu.h")
 
-DC_OK, DC_EINVAL, DC_EDRY, DC_ENONFINITE, DC_ERUNAWAY, DC_EALIGN, DC_ECUDA, DC_ESTATE = range(8)
+(DC_OK, DC_EINVAL, DC_EDRY, DC_ENONFINITE, DC_ERUNAWAY, DC_EALIGN, DC_ECUDA, DC_ESTATE, DC_EIO,
+ DC_ECOLLAPSE) = range(10)
 DC_NOISE_PHILOX, DC_NOISE_INJECTED = 0, 1
 
 STATUS_NAMES = {
     DC_OK: "DC_OK", DC_EINVAL: "DC_EINVAL", DC_EDRY: "DC_EDRY", DC_ENONFINITE: "DC_ENONFINITE",
     DC_ERUNAWAY: "DC_ERUNAWAY", DC_EALIGN: "DC_EALIGN", DC_ECUDA: "DC_ECUDA",
-    DC_ESTATE: "DC_ESTATE",
+    DC_ESTATE: "DC_ESTATE", DC_EIO: "DC_EIO", DC_ECOLLAPSE: "DC_ECOLLAPSE",
 }
 
 
@@ -40,6 +41,13 @@ class DcObs(C.Structure):
     _fields_ = [("x", C.c_double), ("y", C.c_double), ("y_hu", C.c_double), ("y_hv", C.c_double)]
 
 
+class DcObsRecord(C.Structure):
+    """dc_obs_record: one line of the observation file."""
+
+    _fields_ = [("time", C.c_double), ("kind", C.c_int32), ("id", C.c_int32),
+                ("x", C.c_double), ("y", C.c_double), ("y_hu", C.c_double), ("y_hv", C.c_double)]
+
+
 class DcParticleDiag(C.Structure):
     _fields_ = [("c", C.c_double), ("phi", C.c_double), ("gamma", C.c_double),
                 ("zeta", C.c_double), ("alpha", C.c_double)]
@@ -55,6 +63,10 @@ EXPORTS = [
     "dc_drifters_get", "dc_precompute_S", "dc_precompute_local_svd", "dc_iewpf_begin",
     "dc_iewpf_finish", "dc_iewpf_assimilate", "dc_iewpf_diagnostics", "dc_da_cycle",
     "dc_kernel_launches", "dc_stream", "dc_selftest_math", "dc_counters", "dc_time_stages",
+    "dc_drifters_count", "dc_get_config", "dc_save_snapshot", "dc_load_snapshot",
+    "dc_checkpoint_save", "dc_checkpoint_load", "dc_obs_noise", "dc_observe_drifters",
+    "dc_pf_loglik", "dc_pf_weights", "dc_residual_resample", "dc_resample_members",
+    "dc_forecast_error", "dc_obs_file_write", "dc_obs_file_read", "dc_trajectory_write",
 ]
 
 
@@ -119,6 +131,23 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "dc_selftest_math": (st, [C.c_int32, C.POINTER(C.c_uint64)]),
         "dc_counters": (st, [vp, C.POINTER(C.c_uint64)]),
         "dc_time_stages": (st, [vp, C.c_int32, dp]),
+        "dc_drifters_count": (st, [vp, ip]),
+        "dc_get_config": (st, [vp, cfgp, ip, C.POINTER(C.c_int64)]),
+        "dc_save_snapshot": (st, [vp, C.c_int32, C.c_char_p]),
+        "dc_load_snapshot": (st, [vp, C.c_int32, C.c_char_p]),
+        "dc_checkpoint_save": (st, [vp, C.c_char_p, C.c_uint64]),
+        "dc_checkpoint_load": (st, [vp, C.c_char_p, C.POINTER(C.c_uint64)]),
+        "dc_obs_noise": (st, [vp, C.c_int32, ip, C.c_int32, C.c_uint64, C.c_double, C.c_double,
+                              dp]),
+        "dc_observe_drifters": (st, [vp, dp, dp, C.c_int32, C.c_double, dp, dp]),
+        "dc_pf_loglik": (st, [vp, obsp, C.c_int32, C.c_double, C.c_double, dp]),
+        "dc_pf_weights": (st, [dp, C.c_int32, dp, dp]),
+        "dc_residual_resample": (st, [dp, C.c_int32, C.c_uint64, C.c_uint64, ip]),
+        "dc_resample_members": (st, [vp, ip]),
+        "dc_forecast_error": (st, [vp, dp, dp, dp, dp, dp]),
+        "dc_obs_file_write": (st, [C.c_char_p, C.POINTER(DcObsRecord), C.c_int32, C.c_int32]),
+        "dc_obs_file_read": (st, [C.c_char_p, C.POINTER(DcObsRecord), C.c_int32, ip]),
+        "dc_trajectory_write": (st, [vp, C.c_char_p, C.c_double, C.c_int32]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

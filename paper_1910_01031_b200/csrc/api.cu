@@ -335,6 +335,11 @@ __global__ void count_iters_kernel(const int* sub, int M, unsigned long long* ac
         acc[1] += q;
     }
 }
+// error hook for the host-side modules layered on the C ABI (io.cpp)
+dc_status ctx_error(dc_ctx* ctx, dc_status st, const std::string& msg, int m) {
+    return set_err(ctx, st, msg, m);
+}
+
 } // namespace dcg
 
 extern "C" {
@@ -748,6 +753,14 @@ dc_status dc_add_q_half(dc_ctx* ctx, const int32_t* offsets, const double* coars
     return DC_OK;
 }
 
+dc_status dc_get_config(dc_ctx* ctx, dc_config* cfg, int32_t* n_members, int64_t* member_base) {
+    if (!ctx) return DC_ESTATE;
+    if (cfg) *cfg = ctx->cfg;
+    if (n_members) *n_members = ctx->M;
+    if (member_base) *member_base = ctx->base;
+    return DC_OK;
+}
+
 dc_status dc_get_draw_counter(dc_ctx* ctx, uint64_t* d) {
     *d = ctx->me_draw;
     return DC_OK;
@@ -836,3 +849,4 @@ dc_status dc_selftest_math(int32_t device, uint64_t* counts) {
 
 // IEWPF / observation entry points live in iewpf_api.cu; they need the context layout.
 #include "iewpf_api.inc"
+#include "experiment_api.inc"

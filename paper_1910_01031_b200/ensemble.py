@@ -13,7 +13,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._lib import DcConfig, DcError, DcObs, DcParticleDiag
+from ._lib import DcConfig, DcError, DcObs, DcObsRecord, DcParticleDiag
 
 
 @dataclass
@@ -230,6 +230,61 @@ class Ensemble:
         self._ck(self.L.dc_drifters_get(self.h, _d(pos), _i(wind)))
         return pos, wind
 
+    # ---- snapshots / checkpoints (state.hpp:43-116) ----
+    def save_snapshot(self, m, path):
+        self._ck(self.L.dc_save_snapshot(self.h, m, str(path).encode()))
+
+    def load_snapshot(self, m, path):
+        self._ck(self.L.dc_load_snapshot(self.h, m, str(path).encode()))
+
+    def checkpoint_save(self, directory, filter_cycle=0):
+        self._ck(self.L.dc_checkpoint_save(self.h, str(directory).encode(), filter_cycle))
+
+    def checkpoint_load(self, directory) -> int:
+        c = C.c_uint64(0)
+        self._ck(self.L.dc_checkpoint_load(self.h, str(directory).encode(), C.byref(c)))
+        return int(c.value)
+
+    # ---- twin experiment ----
+    def obs_noise(self, kind, ids, obs_index, r_hu=1.0, r_hv=1.0):
+        """eps ~ N(0, diag(r_hu, r_hv)) for platforms (kind, ids) at observation index."""
+        ids = np.ascontiguousarray(ids, np.int32).reshape(-1)
+        out = np.empty((ids.size, 2), np.float64)
+        self._ck(self.L.dc_obs_noise(self.h, kind, _i(ids), ids.size, obs_index, r_hu, r_hv,
+                                     _d(out)))
+        return out
+
+    def observe_drifters(self, prev_xy, cur_xy, dt_obs, eps=None):
+        p = np.ascontiguousarray(prev_xy, np.float64).reshape(-1, 2)
+        c = np.ascontiguousarray(cur_xy, np.float64).reshape(-1, 2)
+        e = None if eps is None else np.ascontiguousarray(eps, np.float64).reshape(-1, 2)
+        out = np.empty_like(p)
+        self._ck(self.L.dc_observe_drifters(self.h, _d(p), _d(c), p.shape[0], dt_obs,
+                                            None if e is None else _d(e), _d(out)))
+        return out
+
+    def pf_loglik(self, obs, r_hu=1.0, r_hv=1.0):
+        arr = obs_array(obs)
+        n = len(np.asarray(obs).reshape(-1, 4))
+        out = np.empty(self.n, np.float64)
+        self._ck(self.L.dc_pf_loglik(self.h, arr, n, r_hu, r_hv, _d(out)))
+        return out
+
+    def resample_members(self, idx):
+        idx = np.ascontiguousarray(idx, np.int32).reshape(self.n)
+        self._ck(self.L.dc_resample_members(self.h, _i(idx)))
+
+    def forecast_error(self, truth_xy):
+        t = np.ascontiguousarray(truth_xy, np.float64).reshape(-1, 2)
+        E, R = C.c_double(0), C.c_double(0)
+        ed = np.empty(t.shape[0], np.float64)
+        rd = np.empty(t.shape[0], np.float64)
+        self._ck(self.L.dc_forecast_error(self.h, _d(t), C.byref(E), C.byref(R), _d(ed), _d(rd)))
+        return E.value, R.value, ed, rd
+
+    def trajectory_write(self, path, time, append=True):
+        self._ck(self.L.dc_trajectory_write(self.h, str(path).encode(), time, int(append)))
+
     # ---- IEWPF ----
     def iewpf_assimilate(self, obs, S, usig, cycle):
         arr = obs_array(obs)
@@ -298,3 +353,55 @@ def precompute_local_svd(cfg: Config, S):
     if rc:
         raise DcError(rc, "dc_precompute_local_svd failed")
     return b, u
+
+
+def pf_weights(loglik, strict=True):
+    """standard_pf_weights normalisation: returns (w, max_loglik).
+    Every exp(loglik) underflowing is the spec's "ensemble collapse": raised as
+    DcError(DC_ECOLLAPSE) when strict, else the max-shifted weights are returned anyway
+    (what the collapse experiment counts)."""
+    L = _lib.load()
+    ll = np.ascontiguousarray(loglik, np.float64).reshape(-1)
+    w = np.empty_like(ll)
+    mx = C.c_double(0)
+    rc = L.dc_pf_weights(_d(ll), ll.size, _d(w), C.byref(mx))
+    if rc and (strict or rc != _lib.DC_ECOLLAPSE):
+        raise DcError(rc, f"ensemble collapse (max log-weight {mx.value:.6g})")
+    return w, mx.value
+
+
+def residual_resample(w, seed, cycle):
+    """residual_resample: ascending index multiset of len(w)."""
+    L = _lib.load()
+    w = np.ascontiguousarray(w, np.float64).reshape(-1)
+    out = np.empty(w.size, np.int32)
+    rc = L.dc_residual_resample(_d(w), w.size, seed, cycle, _i(out))
+    if rc:
+        raise DcError(rc, "residual_resample: invalid weights")
+    return out
+
+
+def write_obs_file(path, records, append=False):
+    """records: iterable of (time, kind, id, x, y, y_hu, y_hv); kind 0 drifter, 1 mooring."""
+    L = _lib.load()
+    recs = list(records)
+    arr = (DcObsRecord * max(1, len(recs)))()
+    for i, r in enumerate(recs):
+        arr[i] = DcObsRecord(float(r[0]), int(r[1]), int(r[2]), *[float(v) for v in r[3:7]])
+    rc = L.dc_obs_file_write(str(path).encode(), arr, len(recs), int(append))
+    if rc:
+        raise DcError(rc, f"cannot write {path}")
+
+
+def read_obs_file(path):
+    """-> list of (time, kind, id, x, y, y_hu, y_hv)."""
+    L = _lib.load()
+    n = C.c_int32(0)
+    rc = L.dc_obs_file_read(str(path).encode(), None, 0, C.byref(n))
+    if rc:
+        raise DcError(rc, f"cannot read {path}")
+    arr = (DcObsRecord * max(1, n.value))()
+    rc = L.dc_obs_file_read(str(path).encode(), arr, n.value, C.byref(n))
+    if rc:
+        raise DcError(rc, f"cannot read {path}")
+    return [(r.time, r.kind, r.id, r.x, r.y, r.y_hu, r.y_hv) for r in arr[:n.value]]

@@ -114,6 +114,12 @@ class Oracle:
             "orc_solve_alpha": [C.c_double, C.c_double, C.c_double, dp, C.POINTER(C.c_int)],
             "orc_lambert_w0": [C.c_double, dp, C.POINTER(C.c_int)],
             "orc_sync_target_beta": [C.c_int, dp, dp, dp, dp],
+            "orc_obs_noise": [P, C.c_int, ip, C.c_int, C.c_uint64, C.c_double, C.c_double, dp],
+            "orc_observe_drifters": [P, dp, dp, C.c_int, C.c_double, dp, dp],
+            "orc_pf_loglik": [P, fp, fp, fp, C.c_int, dp, C.c_double, C.c_double, dp],
+            "orc_pf_weights": [dp, C.c_int, dp, dp],
+            "orc_residual_resample": [dp, C.c_int, C.c_uint64, C.c_uint64, ip],
+            "orc_forecast_error": [P, C.c_int, C.c_int, dp, ip, dp, dp, dp, dp, dp],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -310,6 +316,57 @@ class Oracle:
         return w.value, b.value
 
 
+    # ---- §8(f): twin experiment ----
+    def obs_noise(self, p, kind, ids, obs_index, r_hu=1.0, r_hv=1.0):
+        ids = np.ascontiguousarray(ids, np.int32).reshape(-1)
+        out = np.empty((ids.size, 2), np.float64)
+        self._ck(self.lib.orc_obs_noise(C.byref(p), kind, iptr(ids), ids.size, obs_index, r_hu,
+                                        r_hv, dptr(out)))
+        return out
+
+    def observe_drifters(self, p, prev, cur, dt_obs, eps=None):
+        prev = np.ascontiguousarray(prev, np.float64).reshape(-1, 2)
+        cur = np.ascontiguousarray(cur, np.float64).reshape(-1, 2)
+        e = None if eps is None else np.ascontiguousarray(eps, np.float64).reshape(-1, 2)
+        out = np.empty_like(prev)
+        self._ck(self.lib.orc_observe_drifters(C.byref(p), dptr(prev), dptr(cur), prev.shape[0],
+                                               dt_obs, None if e is None else dptr(e),
+                                               dptr(out)))
+        return out
+
+    def pf_loglik(self, p, s, obs, r_hu=1.0, r_hv=1.0):
+        obs = np.ascontiguousarray(obs, np.float64).reshape(-1, 4)
+        out = C.c_double()
+        self._ck(self.lib.orc_pf_loglik(C.byref(p), fptr(s.eta), fptr(s.hu), fptr(s.hv),
+                                        obs.shape[0], dptr(obs), r_hu, r_hv, C.byref(out)))
+        return out.value
+
+    def pf_weights(self, loglik):
+        ll = np.ascontiguousarray(loglik, np.float64)
+        w = np.empty_like(ll)
+        mx = C.c_double()
+        rc = self.lib.orc_pf_weights(dptr(ll), ll.size, dptr(w), C.byref(mx))
+        return w, mx.value, rc == 0
+
+    def residual_resample(self, w, seed, cycle):
+        w = np.ascontiguousarray(w, np.float64)
+        out = np.empty(w.size, np.int32)
+        self._ck(self.lib.orc_residual_resample(dptr(w), w.size, seed, cycle, iptr(out)))
+        return out
+
+    def forecast_error(self, p, pos, wind, truth):
+        pos = np.ascontiguousarray(pos, np.float64)
+        wind = np.ascontiguousarray(wind, np.int32)
+        truth = np.ascontiguousarray(truth, np.float64).reshape(-1, 2)
+        n_m, n_d = pos.shape[0], pos.shape[1]
+        E, R = C.c_double(), C.c_double()
+        ed, rd = np.empty(n_d), np.empty(n_d)
+        self._ck(self.lib.orc_forecast_error(C.byref(p), n_m, n_d, dptr(pos), iptr(wind),
+                                             dptr(truth), C.byref(E), C.byref(R), dptr(ed),
+                                             dptr(rd)))
+        return E.value, R.value, ed, rd
+
+
 class Ref:
     """The reference's own operators (oracle/_ref/libdcref.so)."""
 
@@ -339,6 +396,8 @@ class Ref:
             "ref_align_coarse_offset": [P, C.c_int, C.c_int, ip, ip] + E,
             "ref_forecast_threads": [P, C.c_int, C.c_uint64, C.c_int, C.POINTER(C.c_uint8),
                                      C.c_int, fp, fp, fp, dp] + E,
+            "ref_save_snapshot": [P, fp, fp, fp, C.c_double, C.c_char_p] + E,
+            "ref_load_snapshot": [P, C.c_char_p, fp, fp, fp, dp] + E,
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -358,6 +417,18 @@ class Ref:
         rc = fn(*args, buf, 512)
         if rc:
             raise CheckerError(rc, buf.value.decode())
+
+    def save_snapshot(self, p, s, path):
+        self._call(self.lib.ref_save_snapshot, C.byref(p), fptr(s.eta), fptr(s.hu), fptr(s.hv),
+                   s.t, str(path).encode())
+
+    def load_snapshot(self, p, path):
+        s = State.zeros(p.ny, p.nx)
+        t = C.c_double()
+        self._call(self.lib.ref_load_snapshot, C.byref(p), str(path).encode(), fptr(s.eta),
+                   fptr(s.hu), fptr(s.hv), C.byref(t))
+        s.t = t.value
+        return s
 
     def init_double_jet(self, p):
         s = State.zeros(p.ny, p.nx)
