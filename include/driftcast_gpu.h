@@ -119,6 +119,9 @@ dc_status dc_add_q_half(dc_ctx* ctx, const int32_t* offsets, const double* coars
                         double scale);
 dc_status dc_get_draw_counter(dc_ctx* ctx, uint64_t* model_error_draw);
 dc_status dc_set_draw_counter(dc_ctx* ctx, uint64_t model_error_draw);
+/* StreamTag of the context's model-error draws (rng.hpp:15-23): 1 model_error (default,
+ * the ensemble), 3 truth_model_error (the twin experiment's truth run). */
+dc_status dc_set_model_error_tag(dc_ctx* ctx, uint64_t tag);
 
 /* ---- observation system ------------------------------------- */
 /* innovation of every member at n_obs observations -> d[m][o][2]
@@ -208,6 +211,22 @@ dc_status dc_obs_file_read(const char* path, dc_obs_record* recs, int32_t capaci
 /* Trajectory output: "time,particle,drifter,x,y,wind_x,wind_y" for every
  * member's drifter copies, global particle ids. Synchronous. */
 dc_status dc_trajectory_write(dc_ctx* ctx, const char* path, double time, int32_t append);
+
+/* generate_truth on device `device`: a one-member truth run on the
+ * truth_model_error stream (model error after every model step), platforms inserted at
+ * insert_time (drifters on a drifters_x x drifters_y lattice, advected in the truth;
+ * moorings on a moorings_x x moorings_y lattice), one record per platform every
+ * obs_interval (a multiple of model_dt) with eps ~ N(0, diag(r_hu, r_hv)). Writes
+ * dir/observations.txt and dir/truth_<t>.dcst (t = 0, every snapshot_interval or the end);
+ * dir must exist. *n_records = records written. */
+typedef struct dc_truth_plan {
+    double duration, insert_time, obs_interval, snapshot_interval; /* s */
+    int32_t drifters_x, drifters_y;  /* 8 x 8 */
+    int32_t moorings_x, moorings_y;  /* 20 x 12 (0: none) */
+    double r_hu, r_hv;               /* observation error variances (R = I in the paper) */
+} dc_truth_plan;
+dc_status dc_generate_truth(const dc_config* cfg, const dc_truth_plan* plan, const char* dir,
+                            int32_t device, int64_t* n_records);
 
 /* ---- IEWPF --------------------------------------------------- */
 /* precompute_S on the host in fp64: HQH^T and S = (HQH^T+R)^-1,

@@ -923,6 +923,20 @@ int orc_perturb_philox(const orc_params* p, uint64_t member, uint64_t draw, floa
     return q_half_add(p, coarse_of(p, oj, ok), xi.data(), 1.0, eta, hu, hv);
 }
 
+/// perturb_state with the counter-based generator on any stream tag (1 model_error,
+/// 3 truth_model_error), substream 0.
+int orc_perturb_philox_tag(const orc_params* p, uint64_t tag, uint64_t member, uint64_t draw,
+                           float* eta, float* hu, float* hv) {
+    if (p->q0 == 0.0) return O_OK;
+    int rc = check_coarse(p);
+    if (rc) return rc;
+    const size_t nr = static_cast<size_t>(p->nx / p->c_omega) * (p->ny / p->c_omega);
+    std::vector<double> xi(nr);
+    int32_t oj, ok;
+    orc_philox_draw(p, tag, member, 0, draw, &oj, &ok, xi.data());
+    return q_half_add(p, coarse_of(p, oj, ok), xi.data(), 1.0, eta, hu, hv);
+}
+
 /// apply_q_half_T (stochastic.hpp:193-202) after align_coarse_offset (grid.hpp:113-117):
 /// out = SOAR(GB^T dipole) on the grid aligned to cell (j,k); offsets returned.
 int orc_apply_q_half_T(const orc_params* p, double y_hu, double y_hv, int j, int k,

@@ -48,6 +48,16 @@ class DcObsRecord(C.Structure):
                 ("x", C.c_double), ("y", C.c_double), ("y_hu", C.c_double), ("y_hv", C.c_double)]
 
 
+class DcTruthPlan(C.Structure):
+    """dc_truth_plan (generate_truth, SPEC.md:383-391)."""
+
+    _fields_ = [("duration", C.c_double), ("insert_time", C.c_double),
+                ("obs_interval", C.c_double), ("snapshot_interval", C.c_double),
+                ("drifters_x", C.c_int32), ("drifters_y", C.c_int32),
+                ("moorings_x", C.c_int32), ("moorings_y", C.c_int32),
+                ("r_hu", C.c_double), ("r_hv", C.c_double)]
+
+
 class DcParticleDiag(C.Structure):
     _fields_ = [("c", C.c_double), ("phi", C.c_double), ("gamma", C.c_double),
                 ("zeta", C.c_double), ("alpha", C.c_double)]
@@ -67,6 +77,7 @@ EXPORTS = [
     "dc_checkpoint_save", "dc_checkpoint_load", "dc_obs_noise", "dc_observe_drifters",
     "dc_pf_loglik", "dc_pf_weights", "dc_residual_resample", "dc_resample_members",
     "dc_forecast_error", "dc_obs_file_write", "dc_obs_file_read", "dc_trajectory_write",
+    "dc_set_model_error_tag", "dc_generate_truth",
 ]
 
 
@@ -148,6 +159,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "dc_obs_file_write": (st, [C.c_char_p, C.POINTER(DcObsRecord), C.c_int32, C.c_int32]),
         "dc_obs_file_read": (st, [C.c_char_p, C.POINTER(DcObsRecord), C.c_int32, ip]),
         "dc_trajectory_write": (st, [vp, C.c_char_p, C.c_double, C.c_int32]),
+        "dc_set_model_error_tag": (st, [vp, C.c_uint64]),
+        "dc_generate_truth": (st, [cfgp, C.POINTER(DcTruthPlan), C.c_char_p, C.c_int32,
+                                   C.POINTER(C.c_int64)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -38,6 +38,7 @@ struct dc_ctx {
     double* corr = nullptr;
     int* offs = nullptr;
     uint64_t me_draw = 0;
+    uint64_t me_tag = 1;  // StreamTag of the model-error draws (1 model_error, 3 truth)
     // flux_rhs scratch (one member)
     float* rhs = nullptr;
     unsigned long long* gmax = nullptr;
@@ -715,7 +716,7 @@ dc_status dc_perturb(dc_ctx* ctx, int32_t mode, const int32_t* offsets, const do
     if (ctx->cfg.q0 == 0.0) return DC_OK; // stochastic.hpp:167: consumes no randomness
     const int M = ctx->M;
     if (mode == DC_NOISE_PHILOX) {
-        launch_philox_noise(ctx->stream, ctx->ep, M, ctx->cfg.seed, 1 /*model_error*/, ctx->base, 0,
+        launch_philox_noise(ctx->stream, ctx->ep, M, ctx->cfg.seed, ctx->me_tag, ctx->base, 0,
                             ctx->me_draw, ctx->xi, ctx->offs, ctx->ctl.err);
         ctx->me_draw += 1;
     } else if (mode == DC_NOISE_INJECTED) {
@@ -763,6 +764,14 @@ dc_status dc_get_config(dc_ctx* ctx, dc_config* cfg, int32_t* n_members, int64_t
 
 dc_status dc_get_draw_counter(dc_ctx* ctx, uint64_t* d) {
     *d = ctx->me_draw;
+    return DC_OK;
+}
+
+dc_status dc_set_model_error_tag(dc_ctx* ctx, uint64_t tag) {
+    if (tag != 1 && tag != 3)
+        return set_err(ctx, DC_EINVAL, "model-error stream tag must be model_error (1) or "
+                                       "truth_model_error (3)");
+    ctx->me_tag = tag;
     return DC_OK;
 }
 

@@ -200,6 +200,10 @@ class Ensemble:
     def draw_counter(self, v: int):
         self._ck(self.L.dc_set_draw_counter(self.h, v))
 
+    def set_model_error_tag(self, tag: int):
+        """1: model_error (ensemble), 3: truth_model_error (twin-experiment truth)."""
+        self._ck(self.L.dc_set_model_error_tag(self.h, tag))
+
     # ---- observation system ----
     def innovations(self, obs):
         arr = obs_array(obs)
@@ -405,3 +409,23 @@ def read_obs_file(path):
     if rc:
         raise DcError(rc, f"cannot read {path}")
     return [(r.time, r.kind, r.id, r.x, r.y, r.y_hu, r.y_hv) for r in arr[:n.value]]
+
+
+def generate_truth(cfg: Config, out_dir, duration, insert_time=0.0, obs_interval=300.0,
+                   snapshot_interval=0.0, drifters=(8, 8), moorings=(0, 0), r=(1.0, 1.0),
+                   device=0):
+    """generate_truth on the GPU: writes out_dir/observations.txt and
+    out_dir/truth_<t>.dcst; returns the number of observation records."""
+    import os
+    from ._lib import DcTruthPlan
+    L = _lib.load()
+    os.makedirs(out_dir, exist_ok=True)
+    plan = DcTruthPlan(duration, insert_time, obs_interval, snapshot_interval, drifters[0],
+                       drifters[1], moorings[0], moorings[1], r[0], r[1])
+    n = C.c_int64(0)
+    c = cfg.to_c()
+    rc = L.dc_generate_truth(C.byref(c), C.byref(plan), str(out_dir).encode(), device,
+                             C.byref(n))
+    if rc:
+        raise DcError(rc, "generate_truth failed")
+    return int(n.value)

@@ -100,6 +100,7 @@ class Oracle:
             "orc_perturb_injected": [P, C.c_int, C.c_int, dp, fp, fp, fp],
             "orc_philox_draw": [P, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, ip, ip, dp],
             "orc_perturb_philox": [P, C.c_uint64, C.c_uint64, fp, fp, fp],
+            "orc_perturb_philox_tag": [P, C.c_uint64, C.c_uint64, C.c_uint64, fp, fp, fp],
             "orc_apply_q_half_T": [P, C.c_double, C.c_double, C.c_int, C.c_int, dp, ip, ip],
             "orc_locate_cell": [P, C.c_double, C.c_double, ip, ip],
             "orc_observe_state": [P, fp, fp, fp, C.c_double, C.c_double, dp],
@@ -217,6 +218,10 @@ class Oracle:
     def perturb_philox(self, p, s, member, draw):
         self._ck(self.lib.orc_perturb_philox(C.byref(p), member, draw, fptr(s.eta), fptr(s.hu),
                                              fptr(s.hv)))
+
+    def perturb_philox_tag(self, p, s, tag, member, draw):
+        self._ck(self.lib.orc_perturb_philox_tag(C.byref(p), tag, member, draw, fptr(s.eta),
+                                                 fptr(s.hu), fptr(s.hv)))
 
     def apply_q_half_T(self, p, y_hu, y_hv, j, k):
         o = np.zeros(self.nr(p), np.float64)

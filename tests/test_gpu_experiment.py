@@ -194,3 +194,56 @@ def test_trajectory_file(tmp_path):
     t, particle, drifter, x, y, wx, wy = lines[-1].split(",")
     assert float(t) == 60.0 and int(particle) == 12 and int(drifter) == 3
     assert float(x) == gp[2, 3, 0] and float(y) == gp[2, 3, 1] and int(wx) == gw[2, 3, 0]
+
+
+def test_generate_truth_matches_oracle(oracle, tmp_path):
+    """generate_truth: the GPU truth run, its drifter/mooring records and
+    its snapshots equal the oracle's replay of the same definition bit for bit; same seed
+    twice gives byte-identical observation files."""
+    pkg, cfg, p = setup()
+    kw = dict(duration=1800.0, insert_time=600.0, obs_interval=300.0, snapshot_interval=900.0,
+              drifters=(4, 3), moorings=(3, 2), r=(1.0, 2.0))
+    n = pkg.generate_truth(cfg, tmp_path / "a", **kw)
+    assert n == (12 + 6) * 4  # platforms x observation times (900, 1200, 1500, 1800)
+    pkg.generate_truth(cfg, tmp_path / "b", **kw)
+    fa = (tmp_path / "a" / "observations.txt").read_bytes()
+    assert fa == (tmp_path / "b" / "observations.txt").read_bytes()
+    recs = pkg.read_obs_file(tmp_path / "a" / "observations.txt")
+    # oracle replay: init, then per 60 s step: drifters, model step, truth model error
+    s = oracle.init_double_jet(p)
+    lx, ly = p.nx * p.dx, p.ny * p.dy
+    lat = lambda a, b: np.array([[(i + 0.5) / a * lx, (j + 0.5) / b * ly]  # noqa: E731
+                                 for j in range(b) for i in range(a)])
+    moor = lat(3, 2)
+    want, pos, prev, k = [], None, None, 0
+    for step in range(31):
+        if step == 10:
+            pos = lat(4, 3)
+            prev = pos.copy()
+        if step > 10 and (step - 10) % 5 == 0:
+            t = step * 60.0
+            eps = oracle.obs_noise(p, 0, np.arange(12), k, 1.0, 2.0)
+            y = oracle.observe_drifters(p, prev, pos, 300.0, eps)
+            want += [(t, 0, i, pos[i, 0], pos[i, 1], y[i, 0], y[i, 1]) for i in range(12)]
+            prev = pos.copy()
+            eps = oracle.obs_noise(p, 1, np.arange(6), k, 1.0, 2.0)
+            for i in range(6):
+                ym = oracle.observe_mooring(p, s, moor[i, 0], moor[i, 1])
+                want.append((t, 1, i, moor[i, 0], moor[i, 1], ym[0] + eps[i, 0],
+                             ym[1] + eps[i, 1]))
+            k += 1
+        if step in (15, 30):
+            g = pkg.Ensemble(cfg, 1)
+            g.load_snapshot(0, tmp_path / "a" / f"truth_{step * 60}.dcst")
+            ge, gu, gv, gt = g.download()
+            assert np.array_equal(ge[0], s.eta) and np.array_equal(gv[0], s.hv)
+            assert gt[0] == step * 60.0
+        if step == 30:
+            break
+        if pos is not None:
+            oracle.advect_drifters(p, s, pos, 60.0)
+        oracle.model_step(p, s, 1)
+        oracle.perturb_philox_tag(p, s, 3, 0, step)
+    assert len(recs) == len(want)
+    for a, b in zip(recs, want):
+        assert a[:3] == b[:3] and all(np.float64(x) == np.float64(y) for x, y in zip(a[3:], b[3:]))
