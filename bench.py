@@ -76,27 +76,27 @@ def platforms(cfg, kind):
 
 
 def synthetic_observations(pkg, cfg, n_cycles, kind, device, stream):
-    """Twin-experiment truth on the GPU: one member on its own stream family (global id
-    10^6), stepped cycle by cycle with model error; drifters advected in the truth;
-    observations y = H_eq*(hu,hv)/(H_eq+eta) at each platform (observe_mooring,
-    SPEC.md:353-361) + N(0, R=I). Returns [n_cycles][n_obs][4] (x, y, y_hu, y_hv)."""
-    truth = pkg.Ensemble(cfg, 1, member_base=10**6, device=device, stream=stream)
-    truth.init_double_jet()
-    pos = platforms(cfg, kind)
-    moving = kind == "drifters"
-    if moving:
-        truth.drifters_set(pos[None])
-    rng = np.random.default_rng(2024)
-    out = []
-    for _ in range(n_cycles):
-        truth.da_cycle(5, np.zeros((0, 4)), np.eye(2), np.eye(49), 0)
-        if moving:
-            p, _ = truth.drifters_get()
-            pos = p[0]
-        y = truth.observe_mooring(0, pos) + rng.normal(0.0, 1.0, size=(len(pos), 2))
-        out.append(np.hstack([pos, y]))
-    truth.close()
-    return np.array(out)
+    """Twin-experiment observations from the library's own generate_truth
+    on this GPU: the truth on the truth_model_error stream with model error every step,
+    64 drifters (displacement observations, observe_drifter) or 240 moorings
+    (observe_mooring) every 300 s from t = 0, eps ~ N(0, R=I) on the obs_noise streams,
+    written to and read back from the observation file. Returns [n_cycles][n_obs][4]
+    (x, y, y_hu, y_hv)."""
+    import shutil
+    import tempfile
+    d = tempfile.mkdtemp(prefix="dc_truth_")
+    try:
+        drifters, moorings = ((8, 8), (0, 0)) if kind == "drifters" else ((0, 0), (20, 12))
+        pkg.generate_truth(cfg, d, duration=300.0 * n_cycles, insert_time=0.0,
+                           obs_interval=300.0, snapshot_interval=0.0, drifters=drifters,
+                           moorings=moorings, device=device)
+        recs = pkg.read_obs_file(os.path.join(d, "observations.txt"))
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+    by_t = {}
+    for t, _, _, x, y, yh, yv in recs:
+        by_t.setdefault(t, []).append((x, y, yh, yv))
+    return np.array([by_t[t] for t in sorted(by_t)][:n_cycles])
 
 
 class ClockSampler:
@@ -424,7 +424,7 @@ def main():
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32 state (SWE stencil) / f64 covariance + filter scalars",
-        "data": "synthetic: double-jet IC, Philox model error, twin-experiment truth with "
+        "data": "synthetic: double-jet IC, Philox model error, generate_truth twin experiment with "
                 f"{obs_all.shape[1]} {args.obs}, R=I",
         "config": {"workload": ("configs[1]: double-jet IEWPF, 100 members/GPU, 64 drifter obs "
                                 "every 5 min, drifter forecast copies in every member")
