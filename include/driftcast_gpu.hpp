@@ -39,7 +39,10 @@ inline void throw_status(dc_status st, const std::string& msg) {
     case DC_EINVAL: throw std::invalid_argument(msg);
     case DC_EDRY: throw DryCellError(msg);
     case DC_ENONFINITE:
-    case DC_ERUNAWAY: throw std::runtime_error(msg);
+    case DC_ERUNAWAY:
+    case DC_EIO:        // snapshot / file I/O (state.hpp:71-116 throws runtime_error)
+    case DC_ECOLLAPSE:  // standard PF weights: "ensemble collapse"
+        throw std::runtime_error(msg);
     default: throw std::runtime_error("driftcast_gpu: " + msg);
     }
 }
@@ -150,6 +153,39 @@ public:
     void upload(int m, const float* eta, const float* hu, const float* hv, double t) {
         check(dc_upload_member(ctx_, m, eta, hu, hv, t));
     }
+    // snapshots / checkpoints (state.hpp:71-116)
+    void save_snapshot(int m, const std::string& path) {
+        check(dc_save_snapshot(ctx_, m, path.c_str()));
+    }
+    void load_snapshot(int m, const std::string& path) {
+        check(dc_load_snapshot(ctx_, m, path.c_str()));
+    }
+    void checkpoint_save(const std::string& dir, std::uint64_t filter_cycle) {
+        check(dc_checkpoint_save(ctx_, dir.c_str(), filter_cycle));
+    }
+    std::uint64_t checkpoint_load(const std::string& dir) {
+        std::uint64_t c = 0;
+        check(dc_checkpoint_load(ctx_, dir.c_str(), &c));
+        return c;
+    }
+
+    // SIR comparison: log-likelihoods of this context's members
+    std::vector<double> pf_loglik(const std::vector<dc_obs>& obs, double r_hu = 1.0,
+                                  double r_hv = 1.0) {
+        std::vector<double> ll(n_);
+        check(dc_pf_loglik(ctx_, obs.data(), static_cast<std::int32_t>(obs.size()), r_hu, r_hv,
+                           ll.data()));
+        return ll;
+    }
+    void resample(const std::vector<std::int32_t>& idx) { check(dc_resample_members(ctx_, idx.data())); }
+
+    // drifter forecast error: {E, RMSE}
+    std::pair<double, double> forecast_error(const std::vector<double>& truth_xy) {
+        double e = 0.0, r = 0.0;
+        check(dc_forecast_error(ctx_, truth_xy.data(), &e, &r, nullptr, nullptr));
+        return {e, r};
+    }
+
     void sync() { check(dc_sync(ctx_)); }
 
 private:
