@@ -716,6 +716,15 @@ dc_status dc_perturb(dc_ctx* ctx, int32_t mode, const int32_t* offsets, const do
     if (ctx->cfg.q0 == 0.0) return DC_OK; // stochastic.hpp:167: consumes no randomness
     const int M = ctx->M;
     if (mode == DC_NOISE_PHILOX) {
+        if (ctx->ep.nxc <= 1280) {  // fused noise + SOAR: xi never goes to HBM
+            launch_philox_soar(ctx->stream, ctx->ep, M, ctx->cfg.seed, ctx->me_tag, ctx->base, 0,
+                               ctx->me_draw, ctx->corr, ctx->offs, ctx->ctl.err);
+            ctx->me_draw += 1;
+            apply_q_half_with_stats(ctx, ctx->offs, 1.0);
+            ctx->launches += 2;
+            CU(cudaGetLastError());
+            return DC_OK;
+        }
         launch_philox_noise(ctx->stream, ctx->ep, M, ctx->cfg.seed, ctx->me_tag, ctx->base, 0,
                             ctx->me_draw, ctx->xi, ctx->offs, ctx->ctl.err);
         ctx->me_draw += 1;

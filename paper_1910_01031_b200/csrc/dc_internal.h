@@ -63,6 +63,11 @@ struct ErrParams {
 void launch_philox_noise(cudaStream_t s, const ErrParams& ep, int M, uint64_t seed, uint64_t tag,
                          int64_t member_base, uint32_t substream, uint64_t draw, double* xi,
                          int* offsets, const int* err);
+// philox_noise + coarse_soar in one pass (xi stays on chip); needs (16+4)*nxc*8 B of
+// shared memory (nxc <= 1280)
+void launch_philox_soar(cudaStream_t s, const ErrParams& ep, int M, uint64_t seed, uint64_t tag,
+                        int64_t member_base, uint32_t substream, uint64_t draw, double* corr,
+                        int* offsets, const int* err);
 void launch_coarse_soar(cudaStream_t s, const ErrParams& ep, int M, const double* in,
                         double* out, const int* err);
 void launch_q_half_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,

@@ -74,6 +74,61 @@ __global__ void coarse_soar_kernel(ErrParams ep, int M, const double* __restrict
     }
 }
 
+// Philox noise + SOAR fused for the model-error draw (perturb_state, stochastic.hpp:164-173):
+// one CTA per (band of kBand coarse rows, member). The band's xi rows and a 2-row periodic
+// halo are generated straight into shared memory (pair p gives elements 2p, 2p+1 as
+// philox_noise does; a pair straddling a row boundary is generated for both rows), then
+// the 5x5 SOAR stencil (db outer, da inner, from 0.0 -- coarse_soar_kernel's order) writes
+// the band of the correlated field. xi never goes to HBM.
+constexpr int kBand = 16;
+
+__global__ void __launch_bounds__(256)
+philox_soar_kernel(ErrParams ep, int M, uint64_t seed, uint64_t tag, long long member_base,
+                   uint32_t substream, uint64_t draw, double* __restrict__ corr,
+                   int* __restrict__ offsets, const int* __restrict__ err) {
+    extern __shared__ double X[];  // [kBand + 4][nxc]
+    const int m = blockIdx.y;
+    if (err && err[m]) return;
+    const uint64_t key = det::stream_key(seed, tag, static_cast<uint64_t>(member_base + m));
+    const int nxc = ep.nxc, nyc = ep.nyc;
+    const int b0 = blockIdx.x * kBand;
+    const int nb = min(kBand, nyc - b0);
+    const int rows = nb + 4;
+    const int ppr = nxc / 2 + 2;  // pair slots per row (covers a row of either parity)
+    for (int it = threadIdx.x; it < rows * ppr; it += blockDim.x) {
+        const int sr = it / ppr, q = it - sr * ppr;
+        const int gb = det::wrapf(b0 - 2 + sr, nyc);
+        const int lo = gb * nxc;                   // first element of the row
+        const int p = (lo >> 1) + q;               // pair index
+        if (2 * p >= lo + nxc) continue;           // past the row
+        double z0, z1;
+        det::normal_pair(key, substream, draw, static_cast<uint32_t>(p), &z0, &z1);
+        const int e0 = 2 * p - lo, e1 = e0 + 1;    // row-local element indices
+        if (e0 >= 0 && e0 < nxc) X[sr * nxc + e0] = z0;
+        if (e1 >= 0 && e1 < nxc) X[sr * nxc + e1] = z1;
+    }
+    if (offsets && blockIdx.x == 0 && threadIdx.x == 0) {
+        int oj, ok;
+        det::draw_offsets(key, substream, draw, ep.c, &oj, &ok);
+        offsets[2 * m] = oj;
+        offsets[2 * m + 1] = ok;
+    }
+    __syncthreads();
+    double* out = corr + static_cast<size_t>(m) * nxc * nyc + static_cast<size_t>(b0) * nxc;
+    for (int i = threadIdx.x; i < nb * nxc; i += blockDim.x) {
+        const int bl = i / nxc, a = i - bl * nxc;
+        double sum = 0.0;
+#pragma unroll
+        for (int db = -2; db <= 2; ++db) {
+            const double* row = X + (bl + 2 + db) * nxc;
+#pragma unroll
+            for (int da = -2; da <= 2; ++da)
+                sum += ep.w[(db + 2) * 5 + (da + 2)] * row[det::wrapf(a + da, nxc)];
+        }
+        out[i] = sum;
+    }
+}
+
 using tile::TX;
 using tile::TY;
 
@@ -209,6 +264,20 @@ void launch_philox_noise(cudaStream_t s, const ErrParams& ep, int M, uint64_t se
     int bx = (npairs + 255) / 256;
     philox_noise_kernel<<<dim3(bx, M), 256, 0, s>>>(ep, M, seed, tag, member_base, substream,
                                                     draw, xi, offsets, err);
+}
+
+void launch_philox_soar(cudaStream_t s, const ErrParams& ep, int M, uint64_t seed, uint64_t tag,
+                        int64_t member_base, uint32_t substream, uint64_t draw, double* corr,
+                        int* offsets, const int* err) {
+    const size_t bytes = static_cast<size_t>(kBand + 4) * ep.nxc * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(philox_soar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+    }
+    philox_soar_kernel<<<dim3((ep.nyc + kBand - 1) / kBand, M), 256, bytes, s>>>(
+        ep, M, seed, tag, member_base, substream, draw, corr, offsets, err);
 }
 
 void launch_coarse_soar(cudaStream_t s, const ErrParams& ep, int M, const double* in,
