@@ -421,44 +421,70 @@ __device__ __forceinline__ int nearest_coarse(int j, int o, int c, int n) {
 }
 
 // Stage 6a: z = beta^1/2 nu + alpha^1/2 xi, then the local U Sigma^1/2 blocks in ascending
-// obs id (overlapping blocks see earlier updates, as the sequential restatement does).
-__global__ void __launch_bounds__(64)
+// obs id. One CTA per member holds z in shared memory; the blocks run
+// level by level (iewpf_api.inc: build_block_schedule) with kLbGroups observations of a
+// level at a time, one 64-thread group each -- the blocks of a level are disjoint, so this
+// equals the sequential ascending-id application bit for bit.
+constexpr int kObsTab = 1024;
+constexpr int kLbGroups = 8;
+
+__global__ void __launch_bounds__(64 * kLbGroups)
 local_blocks_kernel(ErrParams ep, const double* __restrict__ xi, const double* __restrict__ nu,
                     const double* __restrict__ scal, const double* __restrict__ wb,
-                    const int* __restrict__ cells, int n_obs, const int* __restrict__ foffs,
-                    const double* __restrict__ usig, double* z, const int* err) {
+                    const int* __restrict__ cells, int n_obs, const int* __restrict__ order,
+                    const int* __restrict__ level_start, int n_levels,
+                    const int* __restrict__ foffs, const double* __restrict__ usig, double* z,
+                    const int* err, int z_in_smem) {
     const int m = blockIdx.x;
     if (err[m]) return;
-    __shared__ double U[49 * 49];
-    __shared__ double bin[49];
-    __shared__ int idx[49];
+    extern __shared__ double dyn[];  // [49*49] U, then [nr] z when it fits
+    double* U = dyn;
+    __shared__ double bin[kLbGroups][49];
+    __shared__ int idx[kLbGroups][49];
+    __shared__ int ab[kObsTab][2];
+    __shared__ int ord[kObsTab];
+    __shared__ int lst[kObsTab + 1];
     const int nr = ep.nxc * ep.nyc;
     for (int i = threadIdx.x; i < 49 * 49; i += blockDim.x) U[i] = usig[i];
     const double sqb = sqrt(wb[1]);
     const double sqa = sqrt(scal[8 * m + 4]);
     const double* X = xi + static_cast<size_t>(m) * nr;
     const double* N = nu + static_cast<size_t>(m) * nr;
-    double* Z = z + static_cast<size_t>(m) * nr;
+    double* Zg = z + static_cast<size_t>(m) * nr;
+    double* Z = z_in_smem ? dyn + 49 * 49 : Zg;
     for (int i = threadIdx.x; i < nr; i += blockDim.x) Z[i] = sqb * N[i] + sqa * X[i];
     const int oj = foffs[2 * m], ok = foffs[2 * m + 1];
-    __syncthreads();
-    const int r = threadIdx.x;
-    for (int o = 0; o < n_obs; ++o) {
-        const int a0 = nearest_coarse(cells[2 * o], oj, ep.c, ep.nxc);
-        const int b0 = nearest_coarse(cells[2 * o + 1], ok, ep.c, ep.nyc);
-        if (r < 49) {
-            const int id = wrapf(b0 + r / 7 - 3, ep.nyc) * ep.nxc + wrapf(a0 + r % 7 - 3, ep.nxc);
-            idx[r] = id;
-            bin[r] = Z[id];
-        }
-        __syncthreads();
-        if (r < 49) {
-            double s = 0.0;
-            for (int c = 0; c < 49; ++c) s += U[r * 49 + c] * bin[c];
-            Z[idx[r]] = s;
-        }
-        __syncthreads();
+    for (int o = threadIdx.x; o < n_obs; o += blockDim.x) {  // block centres (member offsets)
+        ab[o][0] = nearest_coarse(cells[2 * o], oj, ep.c, ep.nxc);
+        ab[o][1] = nearest_coarse(cells[2 * o + 1], ok, ep.c, ep.nyc);
+        ord[o] = order[o];
     }
+    for (int l = threadIdx.x; l <= n_levels; l += blockDim.x) lst[l] = level_start[l];
+    __syncthreads();
+    const int g = threadIdx.x >> 6, r = threadIdx.x & 63;
+    for (int l = 0; l < n_levels; ++l) {
+        const int le = lst[l + 1];
+        for (int q0 = lst[l]; q0 < le; q0 += kLbGroups) {
+            const bool act = (q0 + g < le) && r < 49;
+            if (act) {
+                const int o = ord[q0 + g];
+                const int id = wrapf(ab[o][1] + r / 7 - 3, ep.nyc) * ep.nxc +
+                               wrapf(ab[o][0] + r % 7 - 3, ep.nxc);
+                idx[g][r] = id;
+                bin[g][r] = Z[id];
+            }
+            __syncthreads();
+            if (act) {
+                double s = 0.0;
+#pragma unroll 7
+                for (int c = 0; c < 49; ++c) s += U[r * 49 + c] * bin[g][c];
+                Z[idx[g][r]] = s;
+            }
+            __syncthreads();
+        }
+    }
+    if (z_in_smem)
+        for (int i = threadIdx.x; i < nr; i += blockDim.x) Zg[i] = Z[i];
 }
 
 // advect_drifters: forward Euler at the containing cell, fp64
@@ -574,8 +600,20 @@ void launch_barrier_alpha(cudaStream_t s, const double* cz_all, int n_total, int
 
 void launch_local_blocks(cudaStream_t s, const ErrParams& ep, const double* xi, const double* nu,
                          const double* scal, const double* wb, const int* cells, int n_obs,
+                         const int* order, const int* level_start, int n_levels,
                          const int* foffs, const double* usig, double* z, const int* err, int M) {
-    local_blocks_kernel<<<M, 64, 0, s>>>(ep, xi, nu, scal, wb, cells, n_obs, foffs, usig, z, err);
+    const size_t nr = static_cast<size_t>(ep.nxc) * ep.nyc;
+    const size_t full = (49 * 49 + nr) * sizeof(double);
+    const int in_smem = full <= 160 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(local_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             160 * 1024);
+        attr = true;
+    }
+    local_blocks_kernel<<<M, 64 * kLbGroups, in_smem ? full : 49 * 49 * sizeof(double), s>>>(
+        ep, xi, nu, scal, wb, cells, n_obs, order, level_start, n_levels, foffs, usig, z, err,
+        in_smem);
 }
 
 void launch_drifters(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,

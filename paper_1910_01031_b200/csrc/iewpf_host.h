@@ -34,6 +34,12 @@ struct IewpfBuffers {
     bool usig_valid = false;
     void* stage = nullptr;    // pinned host staging
     size_t stage_bytes = 0;
+    // local-block schedule: observation ids ordered by dependency level
+    int* lb_order = nullptr;  // [cap_obs]
+    int* lb_start = nullptr;  // [cap_obs + 1] first position of each level in lb_order
+    int lb_levels = 0;
+    std::vector<double> lb_xy;  // observation positions the schedule was built for
+    std::vector<int> lb_host;   // host copy of order + start (source of the async upload)
     // drifters
     int n_d = 0;
     double* dpos = nullptr;   // [M][n_d][2]
@@ -42,7 +48,8 @@ struct IewpfBuffers {
 
 inline void iewpf_free(IewpfBuffers& b) {
     void* ps[] = {b.obs, b.cells, b.d, b.sd, b.win, b.tile_lists, b.tile_count, b.nu, b.scal,
-                  b.cz, b.cz_all, b.wb, b.S, b.usig, b.foffs, b.dpos, b.dwind, b.z, b.bad};
+                  b.cz, b.cz_all, b.wb, b.S, b.usig, b.foffs, b.dpos, b.dwind, b.z, b.bad,
+                  b.lb_order, b.lb_start};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (b.stage) cudaFreeHost(b.stage);
