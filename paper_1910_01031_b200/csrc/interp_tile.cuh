@@ -70,14 +70,12 @@ __device__ __forceinline__ unsigned lanemask_le() {
     return m;
 }
 
-// Tables for one (tile, coarse offset): COLMAP / ROWMAP turn wrapped coarse indices into
-// whatever the value accessor expects. Warp 0 builds the column groups, warp 1 the row
-// groups (one lane per halo row), warp 2 the X-slot rows. Ends with a barrier.
-template <class COLMAP, class ROWMAP>
-__device__ __forceinline__ void setup(Smem& S, const ErrParams& ep, int nx, int ny, int j0,
-                                      int k0, int oj, int ok, COLMAP colmap, ROWMAP rowmap) {
+// Column tables of one tile (warp 0): depend only on the tile's columns and the coarse
+// column offset, so a CTA that streams down a column strip builds them once. No barrier.
+template <class COLMAP>
+__device__ __forceinline__ void setup_cols(Smem& S, const ErrParams& ep, int nx, int j0, int oj,
+                                           COLMAP colmap) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool whole = ep.nyc <= NBMAX;
     if (warp == 0) {  // columns l and 32+l (l < 2) (stochastic.hpp:104-108)
         int a1, a2 = 0;
         double t1, t2 = 0.0;
@@ -118,7 +116,16 @@ __device__ __forceinline__ void setup(Smem& S, const ErrParams& ep, int nx, int 
             S.ncg = n;
             S.cg_first[n] = XW;
         }
-    } else if (warp == 1 || warp == 2) {
+    }
+}
+
+// Row tables of one tile (warps 1, 2). No barrier.
+template <class ROWMAP>
+__device__ __forceinline__ void setup_rows(Smem& S, const ErrParams& ep, int ny, int k0, int ok,
+                                           ROWMAP rowmap) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool whole = ep.nyc <= NBMAX;
+    if (warp == 1 || warp == 2) {
         int bfirst, blast;
         double td;
         row_b0(ep, det::wrap1(k0 - 1, ny), ok, &bfirst, &td);
@@ -153,6 +160,16 @@ __device__ __forceinline__ void setup(Smem& S, const ErrParams& ep, int nx, int 
             if (lane == 0) S.nb = nb;
         }
     }
+}
+
+// Tables for one (tile, coarse offset): COLMAP / ROWMAP turn wrapped coarse indices into
+// whatever the value accessor expects. Warp 0 builds the column groups, warp 1 the row
+// groups (one lane per halo row), warp 2 the X-slot rows. Ends with a barrier.
+template <class COLMAP, class ROWMAP>
+__device__ __forceinline__ void setup(Smem& S, const ErrParams& ep, int nx, int ny, int j0,
+                                      int k0, int oj, int ok, COLMAP colmap, ROWMAP rowmap) {
+    setup_cols(S, ep, nx, j0, oj, colmap);
+    setup_rows(S, ep, ny, k0, ok, rowmap);
     __syncthreads();
 }
 
