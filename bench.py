@@ -174,6 +174,22 @@ def load_peaks():
         return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
+# FP32 lane operations per cell of the exact stage kernels, counted from their SASS
+# (FFMA2/FADD2/FMUL2 = 2, FFMA/FADD/FMUL = 1; tools/sass_hist.py): stage 1, stage 2
+FP32_OPS_PER_CELL = (208.0, 229.0)
+
+
+def fp32_roofline(ms1, ms2, cells, clocks):
+    """Achieved FP32 lane-ops/s of the two stage kernels against B200's FP32 peak
+    (148 SMs x 128 lanes x SM clock under load)."""
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    peak = 148 * 128 * mhz * 1e6 / 1e12
+    achieved = (FP32_OPS_PER_CELL[0] + FP32_OPS_PER_CELL[1]) * cells / ((ms1 + ms2) / 1e3) / 1e12
+    return {"achieved": achieved, "peak": peak, "unit": "T lane-ops/s", "frac": achieved / peak,
+            "ops_per_cell_update": sum(FP32_OPS_PER_CELL),
+            "peak_basis": f"148 SMs x 128 FP32 lanes x {mhz:.0f} MHz"}
+
+
 def profiled_traffic():
     """dram bytes per SWE stage launch from the committed ncu --set full capture."""
     try:
@@ -445,8 +461,9 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "swe_stage (SSP-RK2 stage, 24 B/cell stage 1, 36 B/cell stage 2)",
                      "stage_ms": [ms1, ms2], "peak_source": peak_src,
-                     "note": "the stage kernel is FP32-issue bound (SURVEY.md §7); see "
-                             "profiles/ for issue-slot SOL"},
+                     "note": "the stage kernel is FP32-pipe bound, not HBM bound (DESIGN.md "
+                             "§4): see fp32 for the binding roofline",
+                     "fp32": fp32_roofline(ms1, ms2, cells, clocks)},
         "cpu_baseline": cpu,
         "clocks": clocks,
     }
