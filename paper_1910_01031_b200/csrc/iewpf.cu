@@ -160,23 +160,34 @@ __device__ __forceinline__ bool overlaps(int lo, int hi, int t0, int t1, int n) 
 // grid.hpp:106-117) so the pull does no integer division
 __global__ void tile_lists_kernel(SweParams sp, ErrParams ep, const int* __restrict__ cells,
                                   int n_obs, int tiles_x, int n_tiles, int4* lists, int* counts) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    // one warp per tile; lanes test 32 observations at a time and a ballot prefix keeps
+    // the list in ascending id
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (t >= n_tiles) return;
     const int tx = t % tiles_x, ty = t / tiles_x;
     const int j0 = tx * TX, j1 = min(j0 + TX, sp.nx) - 1;
     const int k0 = ty * TY, k1 = min(k0 + TY, sp.ny) - 1;
     const int r = 7 * ep.c + 1;  // footprint radius
     int n = 0;
-    for (int o = 0; o < n_obs; ++o) {
-        const int jo = cells[2 * o], ko = cells[2 * o + 1];
-        if (overlaps(jo - r, jo + r, j0, j1, sp.nx) && overlaps(ko - r, ko + r, k0, k1, sp.ny)) {
+    for (int base = 0; base < n_obs; base += 32) {
+        const int o = base + lane;
+        bool hit = false;
+        int jo = 0, ko = 0;
+        if (o < n_obs) {
+            jo = cells[2 * o];
+            ko = cells[2 * o + 1];
+            hit = overlaps(jo - r, jo + r, j0, j1, sp.nx) && overlaps(ko - r, ko + r, k0, k1, sp.ny);
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
             const int oj = jo % ep.c, ok = ko % ep.c;
-            lists[static_cast<size_t>(t) * n_obs + n++] =
+            lists[static_cast<size_t>(t) * n_obs + n + __popc(b & ((1u << lane) - 1u))] =
                 make_int4(o, oj | (ok << 16), wrapi((jo - oj) / ep.c, ep.nxc),
                           wrapi((ko - ok) / ep.c, ep.nyc));
         }
+        n += __popc(b);
     }
-    counts[t] = n;
+    if (lane == 0) counts[t] = n;
 }
 
 // Sequential-equivalent gather of every covering observation's pull into one tile of one
@@ -567,8 +578,8 @@ void launch_tile_lists(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
                        int n_obs, int* lists, int* counts, int* n_tiles_out, int* tiles_x_out) {
     const int tiles_x = (sp.nx + TX - 1) / TX, tiles_y = (sp.ny + TY - 1) / TY;
     const int n_tiles = tiles_x * tiles_y;
-    tile_lists_kernel<<<(n_tiles + 127) / 128, 128, 0, s>>>(sp, ep, cells, n_obs, tiles_x, n_tiles,
-                                                           reinterpret_cast<int4*>(lists), counts);
+    tile_lists_kernel<<<(n_tiles * 32 + 127) / 128, 128, 0, s>>>(
+        sp, ep, cells, n_obs, tiles_x, n_tiles, reinterpret_cast<int4*>(lists), counts);
     *n_tiles_out = n_tiles;
     *tiles_x_out = tiles_x;
 }
