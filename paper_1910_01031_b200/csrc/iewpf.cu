@@ -381,20 +381,30 @@ __device__ bool lambert_w0(double x, double* w_out) {
 
 // Stage 4 (the barrier) + stage 5. Single CTA: the sum for w_target and the beta min
 // run in particle-id order over all N_e particles; every rank computes them identically.
+constexpr int kBarrierStage = 2048;  // particles staged in shared memory (32 KB)
+
 __global__ void barrier_alpha_kernel(const double* __restrict__ cz_all, int n_total, int M,
                                      double n_psi, double* scal, double* wb, int* err) {
     __shared__ double s_w, s_b;
     __shared__ int s_bad;
+    // the (c, zeta) pairs are staged in shared memory by all threads, so the fixed-order
+    // sequential reductions below do not wait on a global load per particle
+    __shared__ double cz_s[2 * kBarrierStage];
+    const bool staged = n_total <= kBarrierStage;
+    if (staged)
+        for (int i = threadIdx.x; i < 2 * n_total; i += blockDim.x) cz_s[i] = cz_all[i];
+    __syncthreads();
+    const double* cz = staged ? cz_s : cz_all;
     if (threadIdx.x == 0) {
         double sum = 0.0;
-        for (int i = 0; i < n_total; ++i) sum += cz_all[2 * i];
+        for (int i = 0; i < n_total; ++i) sum += cz[2 * i];
         const double w = sum / n_total;
         double beta = __longlong_as_double(0x7ff0000000000000ll);
         int bad = 0;
         for (int i = 0; i < n_total; ++i) {
-            const double z = cz_all[2 * i + 1];
+            const double z = cz[2 * i + 1];
             if (!(z > 0.0)) bad = 1;
-            const double b = (w - cz_all[2 * i]) / z + 1.0;
+            const double b = (w - cz[2 * i]) / z + 1.0;
             beta = (b < beta) ? b : beta;
         }
         if (!(beta >= 0.0)) bad = 1;

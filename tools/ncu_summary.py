@@ -7,21 +7,22 @@ import sys
 
 
 def kname(full):
-    """'void ns::<unnamed>::foo_kernel<T, 1>(args)' -> 'foo_kernel<T, 1>' (short)."""
-    head = full.replace("dcg::<unnamed>::", "").replace("(anonymous namespace)::", "").split("(")[0]
+    """'void ns::<unnamed>::foo_kernel<(int)1, ns::<unnamed>::PK>(args)' -> 'foo_kernel<1, PK>'."""
+    head = full.replace("dcg::<unnamed>::", "").replace("(anonymous namespace)::", "")
+    head = head.replace("dcg::", "").replace("(int)", "")
     depth, cut = 0, len(head)
-    for i in range(len(head) - 1, -1, -1):  # strip a trailing template argument list
-        if head[i] == ">":
+    for i, ch in enumerate(head):  # cut the argument list: first '(' outside template args
+        if ch == "<":
             depth += 1
-        elif head[i] == "<":
+        elif ch == ">":
             depth -= 1
-            if depth == 0:
-                cut = i
-                break
-    targs = head[cut:].replace("dcg::<unnamed>::", "")
-    parts = head[:cut].split("::")[-1].split()
-    base = parts[-1] if parts else head
-    return base + targs
+        elif ch == "(" and depth == 0:
+            cut = i
+            break
+    head = head[:cut].strip()
+    if head.startswith("void "):
+        head = head[5:]
+    return head
 
 
 def launch_shares(path):
