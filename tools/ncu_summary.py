@@ -9,7 +9,7 @@ import sys
 def kname(full):
     """'void ns::<unnamed>::foo_kernel<(int)1, ns::<unnamed>::PK>(args)' -> 'foo_kernel<1, PK>'."""
     head = full.replace("dcg::<unnamed>::", "").replace("(anonymous namespace)::", "")
-    head = head.replace("dcg::", "").replace("(int)", "")
+    head = head.replace("unnamed>::", "").replace("dcg::", "").replace("(int)", "")
     depth, cut = 0, len(head)
     for i, ch in enumerate(head):  # cut the argument list: first '(' outside template args
         if ch == "<":
