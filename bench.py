@@ -179,6 +179,19 @@ def load_peaks():
 FP32_OPS_PER_CELL = (208.0, 229.0)
 
 
+def workload_name(args, M):
+    """Which BASELINE.json config this run is (configs[1] is the default)."""
+    obs = ("64 drifter obs" if args.obs == "drifters" else "240 moored-buoy obs")
+    if (args.nx, args.ny) == (500, 300):
+        which = "configs[1]" if args.obs == "drifters" else "configs[2]"
+        return (f"{which}: double-jet IEWPF 500x300, {M} members/GPU, {obs} every 5 min, "
+                "drifter forecast copies in every member")
+    if (args.nx, args.ny) == (1000, 600):
+        return (f"configs[4]: double jet refined 2x per axis (1000x600, dx=1110 m), IEWPF, "
+                f"{M} members/GPU, {obs} every 5 min")
+    return f"custom: double-jet IEWPF {args.nx}x{args.ny}, {M} members/GPU, {obs}"
+
+
 def fp32_roofline(ms1, ms2, cells, clocks):
     """Achieved FP32 lane-ops/s of the two stage kernels against B200's FP32 peak
     (148 SMs x 128 lanes x SM clock under load)."""
@@ -255,7 +268,7 @@ def run_reference(args, rank, world):
         return
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from checkers import Oracle, make_params
-    p = make_params(nx=args.nx, ny=args.ny)
+    p = make_params(nx=args.nx, ny=args.ny, dx=2220.0 * 500 / args.nx, dy=2220.0 * 500 / args.nx)
     threads = os.cpu_count() or 1
     sample = max(2, threads)
     orc = Oracle()
@@ -316,7 +329,8 @@ def main():
         else:
             dist.init_process_group(backend)
     stream = torch.cuda.Stream()
-    cfg = pkg.Config(nx=args.nx, ny=args.ny, exact_fp=not args.fast)
+    dx = 2220.0 * 500 / args.nx  # the double-jet domain is fixed; refining shrinks dx
+    cfg = pkg.Config(nx=args.nx, ny=args.ny, dx=dx, dy=dx, exact_fp=not args.fast)
     M = args.members
     K, W = args.steps, args.warmup
     total = M * world
@@ -416,7 +430,7 @@ def main():
         try:
             sys.path.insert(0, os.path.join(ROOT, "tests"))
             from checkers import Oracle, make_params
-            p = make_params(nx=cfg.nx, ny=cfg.ny)
+            p = make_params(nx=cfg.nx, ny=cfg.ny, dx=cfg.dx, dy=cfg.dy)
             threads = os.cpu_count() or 1
             sample = max(2, min(threads, 16))
             base = Oracle().init_double_jet(p)
@@ -442,11 +456,7 @@ def main():
         "dtype": "f32 state (SWE stencil) / f64 covariance + filter scalars",
         "data": "synthetic: double-jet IC, Philox model error, generate_truth twin experiment with "
                 f"{obs_all.shape[1]} {args.obs}, R=I",
-        "config": {"workload": ("configs[1]: double-jet IEWPF, 100 members/GPU, 64 drifter obs "
-                                "every 5 min, drifter forecast copies in every member")
-                   if args.obs == "drifters" else
-                   ("configs[2]: double-jet IEWPF, 100 members/GPU, 240 moored-buoy obs every "
-                    "5 min, drifter forecast copies in every member"),
+        "config": {"workload": workload_name(args, M),
                    "nx": cfg.nx, "ny": cfg.ny, "members_per_gpu": M, "members_total": total,
                    "n_obs": int(obs_all.shape[1]), "obs": args.obs, "cycle": "5 x 60 s steps, "
                    "model error after 4, IEWPF analysis", "exact_fp": not args.fast,
