@@ -461,7 +461,9 @@ def main():
                    "n_obs": int(obs_all.shape[1]), "obs": args.obs, "cycle": "5 x 60 s steps, "
                    "model error after 4, IEWPF analysis", "exact_fp": not args.fast,
                    "parallelism": f"ensemble dp{world}",
-                   "l2": "inputs larger than L2 (state 3 x 100 x 300 x 512 x 4 B x 2 = 368 MB)"},
+                   "l2": f"inputs larger than L2: the state + stage buffers are 6 x {M} x {cfg.ny} x "
+                         f"{(cfg.nx + 31) // 32 * 32} x 4 B = "
+                         f"{6 * M * cfg.ny * ((cfg.nx + 31) // 32 * 32) * 4 / 1e6:.0f} MB vs 126 MB L2"},
         "cycle_ms": ms / K,
         "cell_model_steps_per_s": value / max(1.0, cell_updates / (K * 5 * total * cfg.nx * cfg.ny)),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": obs_bytes,
