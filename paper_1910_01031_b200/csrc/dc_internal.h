@@ -28,7 +28,9 @@ enum DevErr : int {
 // derives them (double, then one rounding to float): swe.hpp:277-278,340-344,356-357,380-382.
 struct SweParams {
     int nx, ny, pitch, M;
-    int by, strips;       // rows per CTA strip, strips per member
+    int by, strips;       // rows per CTA strip, strips per member (uniform strips)
+    const int2* units;    // optional CTA row units {m, y0 | y1 << 16}: big strips first,
+    int n_units;          // short ones last so the final wave drains quickly (api.cu)
     float H, g, theta, cf_x, cf_y, inv_g, idx, idy, fH;
     double dx, dy, courant, model_dt, h_eq, gd;
     float neg_zero;       // -0.0f, opaque to ptxas (packed-product addend, swe.cu)
