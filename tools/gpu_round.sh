@@ -19,7 +19,7 @@ if python tools/profile_cycle.py --cycles 2 > $O/profile_cycle.log 2>&1; then
   ncu --set full --clock-control none --import-source on -k regex:swe_stage_pair -c 2 \
       -o $O/full_swe_${TAG} -f python tools/profile_cycle.py --cycles 1 > $O/ncu_full_swe.log 2>&1
   echo "ncu full swe rc=$?"
-  for k in q_half_apply pull_apply local_blocks cfl_scan; do
+  for k in q_half_apply pull_apply local_blocks philox_soar; do
     ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
         -o $O/full_${k}_${TAG} -f python tools/profile_cycle.py --cycles 1 > $O/ncu_full_$k.log 2>&1
     echo "ncu full $k rc=$?"

@@ -79,7 +79,7 @@ def main(tag):
                "kernels": sh}, open(os.path.join(prof, "r1_launches_cycle.json"), "w"), indent=1)
     groups = {"swe": "r1_swe_stage_ncu.json", "q_half_apply": "r1_perturb_ncu.json",
               "pull_apply": "r1_analysis_ncu.json", "local_blocks": "r1_local_blocks_ncu.json",
-              "cfl_scan": "r1_cfl_scan_ncu.json"}
+              "philox_soar": "r1_philox_soar_ncu.json", "cfl_scan": "r1_cfl_scan_ncu.json"}
     for key, fn in groups.items():
         rep = os.path.join(g, f"full_{key}_{tag}.ncu-rep")
         if not os.path.exists(rep):
