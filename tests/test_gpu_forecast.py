@@ -255,3 +255,28 @@ def test_branch_free_sqrt_rcp_exhaustive():
     assert L.dc_selftest_math(0, counts) == 0
     assert counts[0] == 0, f"sqrt mismatches in [2^-100,2^100]: {counts[0]} (all: {counts[2]})"
     assert counts[1] == 0, f"rcp mismatches in [2^-100,2^100]: {counts[1]} (all: {counts[3]})"
+
+
+@pytest.mark.parametrize("field,value", [("hu", np.nan), ("hv", np.inf)])
+def test_non_finite_state_reported_like_reference(oracle, ref, field, value):
+    """A non-finite transport poisons the substep: the reference's heun sentinel
+    (swe.hpp:99,416-418) throws "model_step: non-finite value after substep k"; the GPU's
+    running packed sentinel reports the same error, substep and member."""
+    _, Ensemble = _gpu()
+    from paper_1910_01031_b200 import DcError
+    cfg, p = cfg_pair(100, 60)
+    eta, hu, hv = perturbed_jets(oracle, p, 3, seed=5)
+    bad = {"hu": hu, "hv": hv}[field]
+    bad[1, 30, 40] = value
+    s = State(eta[1].copy(), hu[1].copy(), hv[1].copy(), 0.0)
+    from checkers import CheckerError
+    with pytest.raises(CheckerError) as er:
+        ref.model_step(p, s, 1)
+    ens = Ensemble(cfg, 3)
+    ens.upload(eta, hu, hv, 0.0)
+    with pytest.raises(DcError) as eg:
+        ens.model_step(1)
+        ens.sync()  # device errors surface at the next synchronising call
+    assert eg.value.status == 3 and eg.value.member == 1
+    assert er.value.msg in eg.value.message, (er.value.msg, eg.value.message)
+    assert eg.value.message.startswith("model_step: non-finite value after substep ")
