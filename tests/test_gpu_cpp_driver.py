@@ -22,7 +22,10 @@ def test_cpp_driver_runs(tmp_path):
            os.path.join(ROOT, "tools", "cpp_driver_example.cpp"), f"-L{lib}", "-ldriftcast_gpu",
            f"-Wl,-rpath,{lib}", "-o", exe]
     subprocess.run(cmd, check=True)
-    out = subprocess.run([exe, "8", "2"], capture_output=True, text=True, timeout=300)
+    out = subprocess.run([exe, "8", "2", str(tmp_path / "ck")], capture_output=True, text=True,
+                         timeout=300)
     assert out.returncode == 0, out.stderr
     assert "cycle 1:" in out.stdout and "invalid_argument caught" in out.stdout
     assert "t = 600.0 s" in out.stdout
+    assert "restart from checkpoint reproduces the run: yes" in out.stdout
+    assert "max PF log-likelihood" in out.stdout

@@ -51,6 +51,23 @@ int main(int argc, char** argv) {
     double t = 0.0;
     ens.download(0, e, u, v, &t);
     std::printf("t = %.1f s, eta[0] = %.6e\n", t, e[0]);
+    // checkpoint, continue one cycle, restore, repeat it: the two runs agree bit for bit
+    const char* dir = argc > 3 ? argv[3] : "/tmp/dc_cpp_checkpoint";
+    ens.checkpoint_save(dir, static_cast<std::uint64_t>(cycles));
+    ens.da_cycle(5, obs, ops, static_cast<std::uint64_t>(cycles));
+    std::vector<float> e1, u1, v1;
+    ens.download(members - 1, e1, u1, v1, &t);
+    const std::uint64_t c0 = ens.checkpoint_load(dir);
+    ens.da_cycle(5, obs, ops, c0);
+    std::vector<float> e2, u2, v2;
+    ens.download(members - 1, e2, u2, v2, &t);
+    std::printf("restart from checkpoint reproduces the run: %s\n",
+                (e1 == e2 && u1 == u2 && v1 == v2) ? "yes" : "NO");
+    // SIR comparison: standard PF log-likelihoods of the members
+    const std::vector<double> ll = ens.pf_loglik(obs);
+    double lmax = -1e300;
+    for (double x : ll) lmax = std::fmax(lmax, x);
+    std::printf("max PF log-likelihood %.3f\n", lmax);
     // the reference's exception types come back through the shim
     try {
         dc_config bad = cfg;
