@@ -195,13 +195,23 @@ __global__ void tile_lists_kernel(SweParams sp, ErrParams ep, const int* __restr
 constexpr int WP = 16;  // padded window pitch: indices 11..15 read exact zeros
 constexpr int kRowsPerThread = (TY + 7) / 8;
 
-__global__ void __launch_bounds__(tile::NT, 3)
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
+}
+
+#ifndef DC_PULL_MIN_BLOCKS
+#define DC_PULL_MIN_BLOCKS 6
+#endif
+
+__global__ void __launch_bounds__(tile::NT, DC_PULL_MIN_BLOCKS)
 pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, int n_obs,
                   const int4* __restrict__ lists,
                   const int* __restrict__ counts, int tiles_x, float* eta, float* hu, float* hv,
                   int* err, int* err_pos) {
     __shared__ double W[WP * WP];
     __shared__ tile::Smem S;
+    __shared__ float ST[3][TY][TX];  // the tile's state across all observations
     const int m = blockIdx.y;
     if (err[m]) return;
     const int tl = blockIdx.x;
@@ -209,21 +219,25 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
     if (cnt == 0) return;
     const int j0 = (tl % tiles_x) * TX, k0 = (tl / tiles_x) * TY;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    const int j = j0 + tx;
     const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
-    // the tile's cells live in registers across all observations
-    float e[kRowsPerThread], u[kRowsPerThread], v[kRowsPerThread];
+    // each thread stages (and later owns) its cells in shared memory: registers stay free
+    // for occupancy, and no barrier is needed since only the owner touches them
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = ty + 8 * q, k = k0 + r, j = j0 + tx;
-        const bool okc = (r < TY) && (k < sp.ny) && (j < sp.nx);
-        const size_t o = mbase + static_cast<size_t>(okc ? k : 0) * sp.pitch + (okc ? j : 0);
-        e[q] = okc ? eta[o] : 0.0f;
-        u[q] = okc ? hu[o] : 0.0f;
-        v[q] = okc ? hv[o] : 0.0f;
+        const int r = ty + 8 * q, k = k0 + r;
+        if (r < TY && k < sp.ny && j < sp.nx) {
+            const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
+            cp_async4(&ST[0][r][tx], eta + o);
+            cp_async4(&ST[1][r][tx], hu + o);
+            cp_async4(&ST[2][r][tx], hv + o);
+        }
     }
+    asm volatile("cp.async.commit_group;\n" ::);
     bool dry = false;
     int dry_at = 0x7fffffff;
     const int nxc = ep.nxc, nyc = ep.nyc;
+    const double cy = ep.cy, cx = ep.cx, heq = ep.h_eq;
     for (int li = 0; li < cnt; ++li) {
         const int4 ent = lists[static_cast<size_t>(tl) * n_obs + li];
         const int o = ent.x;
@@ -245,32 +259,33 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
                 return (db < WIN ? db : WP - 1) * WP;
             });
         tile::interpolate(S, [&](int brow, int a) { return W[brow + a]; });
+        if (li == 0) asm volatile("cp.async.wait_group 0;\n" ::);  // own cells landed
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; ++q) {
-            const int r = ty + 8 * q, k = k0 + r, j = j0 + tx;
+            const int r = ty + 8 * q, k = k0 + r;
             if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
             const int rr = r + 1, jl = tx + 1;
             const double de = S.D[rr][jl];
-            const double dhu = -ep.cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
-            const double dhv = ep.cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
-            const double ee = static_cast<double>(e[q]) + 1.0 * de;
-            if (!(ep.h_eq + ee > 0.0)) {
+            const double dhu = -cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
+            const double dhv = cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
+            const double ee = static_cast<double>(ST[0][r][tx]) + 1.0 * de;
+            if (!(heq + ee > 0.0)) {
                 dry = true;
                 dry_at = min(dry_at, k * sp.nx + j);
             }
-            e[q] = static_cast<float>(ee);
-            u[q] = static_cast<float>(static_cast<double>(u[q]) + 1.0 * dhu);
-            v[q] = static_cast<float>(static_cast<double>(v[q]) + 1.0 * dhv);
+            ST[0][r][tx] = static_cast<float>(ee);
+            ST[1][r][tx] = static_cast<float>(static_cast<double>(ST[1][r][tx]) + 1.0 * dhu);
+            ST[2][r][tx] = static_cast<float>(static_cast<double>(ST[2][r][tx]) + 1.0 * dhv);
         }
     }
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = ty + 8 * q, k = k0 + r, j = j0 + tx;
+        const int r = ty + 8 * q, k = k0 + r;
         if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
         const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
-        eta[o] = e[q];
-        hu[o] = u[q];
-        hv[o] = v[q];
+        eta[o] = ST[0][r][tx];
+        hu[o] = ST[1][r][tx];
+        hv[o] = ST[2][r][tx];
     }
     if (dry) {
         atomicCAS(err + m, 0, E_DRY_ADD);
