@@ -72,6 +72,13 @@ typedef struct dc_particle_diag {
     double c, phi, gamma, zeta, alpha;
 } dc_particle_diag;
 
+/* IEWPF variant: the two-stage scheme of the paper (default) or the
+ * original one-stage IEWPF (target weight max c_i, update alpha^1/2 P^1/2 xi). */
+typedef enum dc_iewpf_mode {
+    DC_IEWPF_TWO_STAGE = 0,
+    DC_IEWPF_ONE_STAGE = 1
+} dc_iewpf_mode;
+
 typedef struct dc_ctx dc_ctx;
 
 /* ---- lifetime ------------------------------------------------------------------ */
@@ -248,6 +255,10 @@ dc_status dc_iewpf_begin(dc_ctx* ctx, const dc_obs* obs, int32_t n_obs, const do
  * cz_is_device): barrier scalars, alpha, P^{1/2} posterior update. */
 dc_status dc_iewpf_finish(dc_ctx* ctx, const void* cz_all, int32_t cz_is_device);
 /* Single-context convenience: begin + finish without a collective (n_total = n_members). */
+/* Select the IEWPF variant for the following analyses (default DC_IEWPF_TWO_STAGE).
+ * One-stage: w_target = max_i c_i, c*_i = w_target - c_i, posterior
+ * psi^a + alpha^1/2 P^1/2 xi; the reported beta is 0. */
+dc_status dc_iewpf_set_mode(dc_ctx* ctx, int32_t mode);
 dc_status dc_iewpf_assimilate(dc_ctx* ctx, const dc_obs* obs, int32_t n_obs, const double* S,
                               const double* usig, uint64_t cycle);
 /* Diagnostics of the last analysis (synchronous): per particle + (w_target, beta). */

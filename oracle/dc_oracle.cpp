@@ -36,6 +36,7 @@ namespace {
 enum { O_OK = 0, O_EINVAL = 1, O_EDRY = 2, O_ENONFINITE = 3, O_ERUNAWAY = 4, O_EALIGN = 5 };
 
 thread_local std::string g_err;
+bool g_one_stage = false;  // orc_iewpf_set_mode
 
 int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -762,6 +763,9 @@ extern "C" {
 
 const char* orc_last_error() { return g_err.c_str(); }
 
+/// IEWPF variant used by orc_iewpf_assimilate: 0 two-stage (default), 1 one-stage.
+void orc_iewpf_set_mode(int one_stage) { g_one_stage = one_stage != 0; }
+
 /// init_double_jet restated (swe.hpp:459-500) with default JetParams.
 int orc_init_double_jet(const orc_params* p, float* eta, float* hu, float* hv) {
     const int ny = p->ny;
@@ -1177,19 +1181,28 @@ int orc_iewpf_assimilate(const orc_params* p, int n_local, uint64_t member_base,
         }
         return O_OK;
     }
-    // stage 4: barrier -- w_target = mean c, beta = min((w-c)/zeta + 1), id order
+    // stage 4: barrier -- w_target = mean c, beta = min((w-c)/zeta + 1), id order.
+    // One-stage IEWPF: w_target = max c, no nu term (beta 0).
     const double* call = c_all ? c_all : cvec.data();
     const double* zall = zeta_all ? zeta_all : zet.data();
-    double sum = 0.0;
-    for (int i = 0; i < n_total; ++i) sum += call[i];
-    const double w_target = sum / n_total;
-    double beta = std::numeric_limits<double>::infinity();
-    for (int i = 0; i < n_total; ++i) {
-        if (!(zall[i] > 0.0)) return fail(O_EINVAL, "sync_target_beta: zeta <= 0");
-        double b = (w_target - call[i]) / zall[i] + 1.0;
-        beta = (b < beta) ? b : beta;
+    double w_target, beta;
+    if (g_one_stage) {
+        w_target = -std::numeric_limits<double>::infinity();
+        for (int i = 0; i < n_total; ++i) w_target = (call[i] > w_target) ? call[i] : w_target;
+        beta = 0.0;
+    } else {
+        double sum = 0.0;
+        for (int i = 0; i < n_total; ++i) sum += call[i];
+        w_target = sum / n_total;
+        beta = std::numeric_limits<double>::infinity();
+        for (int i = 0; i < n_total; ++i) {
+            if (!(zall[i] > 0.0)) return fail(O_EINVAL, "sync_target_beta: zeta <= 0");
+            double b = (w_target - call[i]) / zall[i] + 1.0;
+            beta = (b < beta) ? b : beta;
+        }
+        if (!(beta >= 0.0))
+            return fail(O_EINVAL, "sync_target_beta: beta < 0 (beta^1/2 not real)");
     }
-    if (!(beta >= 0.0)) return fail(O_EINVAL, "sync_target_beta: beta < 0 (beta^1/2 not real)");
     if (diag_g) {
         diag_g[0] = w_target;
         diag_g[1] = beta;
@@ -1198,7 +1211,8 @@ int orc_iewpf_assimilate(const orc_params* p, int n_local, uint64_t member_base,
     std::vector<double> z(nr), blk_in(49), blk_out(49);
     for (int i = 0; i < n_local; ++i) {
         // stage 5: c* and alpha
-        const double cstar = (w_target - cvec[i]) - (beta - 1.0) * zet[i];
+        const double cstar = g_one_stage ? w_target - cvec[i]
+                                         : (w_target - cvec[i]) - (beta - 1.0) * zet[i];
         double alpha;
         int clamped;
         rc = solve_alpha(cstar, gam[i], n_psi, &alpha, &clamped);
@@ -1213,7 +1227,8 @@ int orc_iewpf_assimilate(const orc_params* p, int n_local, uint64_t member_base,
         // stage 6: z = beta^1/2 nu + alpha^1/2 xi; local U Sigma^1/2 blocks in id order;
         // then Q^1/2 and add
         const double sqa = std::sqrt(alpha);
-        for (size_t q = 0; q < nr; ++q) z[q] = sqb * nus[i][q] + sqa * xis[i][q];
+        for (size_t q = 0; q < nr; ++q)
+            z[q] = g_one_stage ? sqa * xis[i][q] : sqb * nus[i][q] + sqa * xis[i][q];
         for (int o = 0; o < n_obs; ++o) {
             const int a0 = nearest_coarse(cj[o], f_oj[i], c, nxc);
             const int b0 = nearest_coarse(ck[o], f_ok[i], c, nyc);

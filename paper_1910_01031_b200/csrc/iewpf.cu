@@ -398,8 +398,12 @@ __device__ bool lambert_w0(double x, double* w_out) {
 // run in particle-id order over all N_e particles; every rank computes them identically.
 constexpr int kBarrierStage = 2048;  // particles staged in shared memory (32 KB)
 
+// Stage 4 + 5. Two-stage (default): w_target = mean c, beta = min((w - c)/zeta + 1),
+// c* = (w - c) - (beta - 1) zeta. One-stage IEWPF:
+// w_target = max c, c* = w - c, no nu term (beta reported as 0).
 __global__ void barrier_alpha_kernel(const double* __restrict__ cz_all, int n_total, int M,
-                                     double n_psi, double* scal, double* wb, int* err) {
+                                     double n_psi, double* scal, double* wb, int* err,
+                                     int one_stage) {
     __shared__ double s_w, s_b;
     __shared__ int s_bad;
     // the (c, zeta) pairs are staged in shared memory by all threads, so the fixed-order
@@ -411,18 +415,25 @@ __global__ void barrier_alpha_kernel(const double* __restrict__ cz_all, int n_to
     __syncthreads();
     const double* cz = staged ? cz_s : cz_all;
     if (threadIdx.x == 0) {
-        double sum = 0.0;
-        for (int i = 0; i < n_total; ++i) sum += cz[2 * i];
-        const double w = sum / n_total;
-        double beta = __longlong_as_double(0x7ff0000000000000ll);
+        double w, beta;
         int bad = 0;
-        for (int i = 0; i < n_total; ++i) {
-            const double z = cz[2 * i + 1];
-            if (!(z > 0.0)) bad = 1;
-            const double b = (w - cz[2 * i]) / z + 1.0;
-            beta = (b < beta) ? b : beta;
+        if (one_stage) {
+            w = -__longlong_as_double(0x7ff0000000000000ll);
+            for (int i = 0; i < n_total; ++i) w = (cz[2 * i] > w) ? cz[2 * i] : w;
+            beta = 0.0;
+        } else {
+            double sum = 0.0;
+            for (int i = 0; i < n_total; ++i) sum += cz[2 * i];
+            w = sum / n_total;
+            beta = __longlong_as_double(0x7ff0000000000000ll);
+            for (int i = 0; i < n_total; ++i) {
+                const double z = cz[2 * i + 1];
+                if (!(z > 0.0)) bad = 1;
+                const double b = (w - cz[2 * i]) / z + 1.0;
+                beta = (b < beta) ? b : beta;
+            }
+            if (!(beta >= 0.0)) bad = 1;
         }
-        if (!(beta >= 0.0)) bad = 1;
         s_w = w;
         s_b = beta;
         s_bad = bad;
@@ -437,7 +448,7 @@ __global__ void barrier_alpha_kernel(const double* __restrict__ cz_all, int n_to
             continue;
         }
         const double c = scal[8 * m + 0], gamma = scal[8 * m + 2], zeta = scal[8 * m + 3];
-        const double cstar = (s_w - c) - (s_b - 1.0) * zeta;
+        const double cstar = one_stage ? s_w - c : (s_w - c) - (s_b - 1.0) * zeta;
         const double t = gamma / n_psi;
         const double x = -((t * det::exp_det(-t)) * det::exp_det(-cstar / n_psi));
         double w;
@@ -470,7 +481,7 @@ local_blocks_kernel(ErrParams ep, const double* __restrict__ xi, const double* _
                     const int* __restrict__ cells, int n_obs, const int* __restrict__ order,
                     const int* __restrict__ level_start, int n_levels,
                     const int* __restrict__ foffs, const double* __restrict__ usig, double* z,
-                    const int* err, int z_in_smem) {
+                    const int* err, int z_in_smem, int one_stage) {
     const int m = blockIdx.x;
     if (err[m]) return;
     extern __shared__ double dyn[];  // [49*49] U, then [nr] z when it fits
@@ -488,7 +499,8 @@ local_blocks_kernel(ErrParams ep, const double* __restrict__ xi, const double* _
     const double* N = nu + static_cast<size_t>(m) * nr;
     double* Zg = z + static_cast<size_t>(m) * nr;
     double* Z = z_in_smem ? dyn + 49 * 49 : Zg;
-    for (int i = threadIdx.x; i < nr; i += blockDim.x) Z[i] = sqb * N[i] + sqa * X[i];
+    for (int i = threadIdx.x; i < nr; i += blockDim.x)
+        Z[i] = one_stage ? sqa * X[i] : sqb * N[i] + sqa * X[i];
     const int oj = foffs[2 * m], ok = foffs[2 * m + 1];
     for (int o = threadIdx.x; o < n_obs; o += blockDim.x) {  // block centres (member offsets)
         ab[o][0] = nearest_coarse(cells[2 * o], oj, ep.c, ep.nxc);
@@ -630,14 +642,15 @@ void launch_gather_cz(cudaStream_t s, int M, const double* scal, double* cz) {
 }
 
 void launch_barrier_alpha(cudaStream_t s, const double* cz_all, int n_total, int M, double n_psi,
-                          double* scal, double* wb, int* err) {
-    barrier_alpha_kernel<<<1, 256, 0, s>>>(cz_all, n_total, M, n_psi, scal, wb, err);
+                          int one_stage, double* scal, double* wb, int* err) {
+    barrier_alpha_kernel<<<1, 256, 0, s>>>(cz_all, n_total, M, n_psi, scal, wb, err, one_stage);
 }
 
 void launch_local_blocks(cudaStream_t s, const ErrParams& ep, const double* xi, const double* nu,
                          const double* scal, const double* wb, const int* cells, int n_obs,
                          const int* order, const int* level_start, int n_levels,
-                         const int* foffs, const double* usig, double* z, const int* err, int M) {
+                         const int* foffs, const double* usig, double* z, const int* err, int M,
+                         int one_stage) {
     const size_t nr = static_cast<size_t>(ep.nxc) * ep.nyc;
     const size_t full = (49 * 49 + nr) * sizeof(double);
     const int in_smem = full <= 160 * 1024;
@@ -649,7 +662,7 @@ void launch_local_blocks(cudaStream_t s, const ErrParams& ep, const double* xi, 
     }
     local_blocks_kernel<<<M, 64 * kLbGroups, in_smem ? full : 49 * 49 * sizeof(double), s>>>(
         ep, xi, nu, scal, wb, cells, n_obs, order, level_start, n_levels, foffs, usig, z, err,
-        in_smem);
+        in_smem, one_stage);
 }
 
 void launch_drifters(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,

@@ -29,6 +29,7 @@ struct IewpfBuffers {
     int* bad = nullptr;       // locate failure flag
     int n_total = 0;
     uint64_t cycle = 0;
+    int one_stage = 0;        // dc_iewpf_set_mode
     double S_host[4] = {0, 0, 0, 0};
     std::vector<double> usig_host;
     bool usig_valid = false;

@@ -290,6 +290,10 @@ class Ensemble:
         self._ck(self.L.dc_trajectory_write(self.h, str(path).encode(), time, int(append)))
 
     # ---- IEWPF ----
+    def iewpf_set_mode(self, one_stage: bool):
+        """one-stage IEWPF (target max c_i) instead of the two-stage default."""
+        self._ck(self.L.dc_iewpf_set_mode(self.h, 1 if one_stage else 0))
+
     def iewpf_assimilate(self, obs, S, usig, cycle):
         arr = obs_array(obs)
         n = len(np.asarray(obs).reshape(-1, 4))

@@ -137,6 +137,8 @@ class Oracle:
         L.orc_det_sincos2pi.restype = None
         L.orc_nearest_coarse.argtypes = [C.c_int] * 4
         L.orc_nearest_coarse.restype = C.c_int
+        L.orc_iewpf_set_mode.argtypes = [C.c_int]
+        L.orc_iewpf_set_mode.restype = None
         L.orc_dot_tree.argtypes = [dp, dp, C.c_int]
         L.orc_dot_tree.restype = C.c_double
 

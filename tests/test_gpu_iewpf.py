@@ -215,3 +215,29 @@ def test_iewpf_dense_platforms_bitwise(oracle):
     oe, ou, ov = e.copy(), u.copy(), v.copy()
     oracle.iewpf_assimilate(p, oe, ou, ov, obs, S, usig, 1)
     assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
+
+
+def test_one_stage_iewpf_bitwise(oracle):
+    """the one-stage variant (target max c_i, alpha^1/2 P^1/2 xi) equals the
+    restatement bit for bit."""
+    pkg, cfg, p = setup()
+    n = 5
+    e, u, v = spread_states(oracle, p, n, 13)
+    obs = obs_set(p, 6, 19)
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    ens.iewpf_set_mode(True)
+    ens.iewpf_assimilate(obs, S, usig, cycle=2)
+    ge, gu, gv, _ = ens.download()
+    diag, wb = ens.iewpf_diagnostics()
+    oe, ou, ov = e.copy(), u.copy(), v.copy()
+    oracle.lib.orc_iewpf_set_mode(1)
+    try:
+        od, owb = oracle.iewpf_assimilate(p, oe, ou, ov, obs, S, usig, 2)
+    finally:
+        oracle.lib.orc_iewpf_set_mode(0)
+    assert np.array_equal(wb, owb) and wb[0] == diag[:, 0].max() and wb[1] == 0.0
+    assert np.array_equal(diag, od)
+    assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)

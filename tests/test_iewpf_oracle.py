@@ -221,3 +221,28 @@ def test_slices_equal_whole(oracle):
         out.append((se, su, sv, d))
     assert np.array_equal(np.concatenate([o[0] for o in out]), we)
     assert np.array_equal(np.concatenate([o[3] for o in out]), dw)
+
+
+def test_one_stage_iewpf(oracle):
+    """One-stage mode: w_target = max c_i, c*_i = w_target - c_i, so the worst particle gets
+    alpha = 1 and every particle reaches the target: (alpha-1) gamma - N log alpha + c = w."""
+    p = make_params(nx=100, ny=60)
+    n = 8
+    e, u, v = _ensemble(oracle, p, n, 2)
+    rng = np.random.default_rng(4)
+    obs = np.hstack([rng.uniform(0, 1, (3, 2)) * [p.nx * p.dx, p.ny * p.dy],
+                     rng.normal(0, 15, (3, 2))])
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    oracle.lib.orc_iewpf_set_mode(1)
+    try:
+        diag, (w, beta) = oracle.iewpf_assimilate(p, e, u, v, obs, S, usig, 0)
+    finally:
+        oracle.lib.orc_iewpf_set_mode(0)
+    n_psi = 3.0 * p.nx * p.ny
+    c, gamma, alpha = diag[:, 0], diag[:, 2], diag[:, 4]
+    assert w == c.max() and beta == 0.0
+    assert abs(alpha[np.argmax(c)] - 1.0) < 1e-9
+    assert np.all((alpha > 0) & (alpha <= 1.0 + 1e-12))
+    lw = (alpha - 1) * gamma - n_psi * np.log(alpha) + c
+    assert np.abs(lw - w).max() <= 1e-6 * abs(w)
