@@ -264,6 +264,12 @@ dc_status dc_iewpf_assimilate(dc_ctx* ctx, const dc_obs* obs, int32_t n_obs, con
 /* Diagnostics of the last analysis (synchronous): per particle + (w_target, beta). */
 dc_status dc_iewpf_diagnostics(dc_ctx* ctx, dc_particle_diag* per_member, double* w_beta);
 
+/* Per-cycle diagnostics dump (SPEC.md iewpf_filter External Interfaces): lines
+ * "cycle,particle,c,gamma,zeta,alpha,beta,w_target" of the last analysis, global particle
+ * ids, %.17g. Synchronous. */
+dc_status dc_iewpf_diagnostics_write(dc_ctx* ctx, const char* path, uint64_t cycle,
+                                     int32_t append);
+
 /* ---- one data-assimilation cycle ----------------------------- */
 /* n_steps model steps; model error (PHILOX) after each but the last; drifters advected
  * by model_dt before each step when drifters are set; then the IEWPF analysis

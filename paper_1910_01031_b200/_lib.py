@@ -78,6 +78,7 @@ EXPORTS = [
     "dc_pf_loglik", "dc_pf_weights", "dc_residual_resample", "dc_resample_members",
     "dc_forecast_error", "dc_obs_file_write", "dc_obs_file_read", "dc_trajectory_write",
     "dc_set_model_error_tag", "dc_generate_truth", "dc_iewpf_set_mode",
+    "dc_iewpf_diagnostics_write",
 ]
 
 
@@ -161,6 +162,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "dc_trajectory_write": (st, [vp, C.c_char_p, C.c_double, C.c_int32]),
         "dc_set_model_error_tag": (st, [vp, C.c_uint64]),
         "dc_iewpf_set_mode": (st, [vp, C.c_int32]),
+        "dc_iewpf_diagnostics_write": (st, [vp, C.c_char_p, C.c_uint64, C.c_int32]),
         "dc_generate_truth": (st, [cfgp, C.POINTER(DcTruthPlan), C.c_char_p, C.c_int32,
                                    C.POINTER(C.c_int64)]),
     }

@@ -288,6 +288,30 @@ dc_status dc_trajectory_write(dc_ctx* ctx, const char* path, double time, int32_
     return DC_OK;
 }
 
+// ---- per-cycle IEWPF diagnostics (SPEC.md iewpf_filter External Interfaces) ----
+// lines "cycle,particle,c,gamma,zeta,alpha,beta,w_target" for the context's members
+dc_status dc_iewpf_diagnostics_write(dc_ctx* ctx, const char* path, uint64_t cycle,
+                                     int32_t append) {
+    if (!ctx || !path) return DC_ESTATE;
+    int32_t M = 0;
+    int64_t base = 0;
+    dc_get_config(ctx, nullptr, &M, &base);
+    std::vector<dc_particle_diag> d(M);
+    double wb[2] = {0.0, 0.0};
+    dc_status st = dc_iewpf_diagnostics(ctx, d.data(), wb);
+    if (st) return st;
+    std::FILE* f = std::fopen(path, append ? "a" : "w");
+    if (!f) return dcg::ctx_error(ctx, DC_EIO, std::string("diagnostics: cannot open ") + path, -1);
+    for (int m = 0; m < M; ++m)
+        std::fprintf(f, "%llu,%lld,%.17g,%.17g,%.17g,%.17g,%.17g,%.17g\n",
+                     static_cast<unsigned long long>(cycle), static_cast<long long>(base + m),
+                     d[m].c, d[m].gamma, d[m].zeta, d[m].alpha, wb[1], wb[0]);
+    const bool ok = std::ferror(f) == 0;
+    if (std::fclose(f) != 0 || !ok)
+        return dcg::ctx_error(ctx, DC_EIO, "diagnostics: write failed", -1);
+    return DC_OK;
+}
+
 dc_status dc_checkpoint_load(dc_ctx* ctx, const char* dir, uint64_t* filter_cycle) {
     if (!ctx || !dir) return DC_ESTATE;
     const std::string d(dir);

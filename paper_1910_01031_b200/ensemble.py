@@ -330,6 +330,10 @@ class Ensemble:
         arr = np.array([[x.c, x.phi, x.gamma, x.zeta, x.alpha] for x in d], np.float64)
         return arr, wb
 
+    def iewpf_diagnostics_write(self, path, cycle, append=True):
+        self._ck(self.L.dc_iewpf_diagnostics_write(self.h, str(path).encode(), cycle,
+                                                   int(append)))
+
     def da_cycle(self, n_steps, obs, S, usig, cycle):
         arr = obs_array(obs)
         n = len(np.asarray(obs).reshape(-1, 4))
