@@ -44,7 +44,7 @@ def main():
     ens.model_step(5)  # forecast to the next observation time
     last = obs[times[a.cycles]]
     rng = np.random.default_rng(6)  # the collapse_subsets stream of this tool
-    print("subset_size,mean_count_w_gt_1_over_Ne")
+    print("subset_size,mean_count_w_ge_1_over_Ne")
     for k in a.sizes:
         counts = []
         for _ in range(a.trials):
@@ -52,7 +52,8 @@ def main():
             ll = ens.pf_loglik(last[idx], r_hu=a.r_scale, r_hv=a.r_scale) if k else \
                 np.zeros(a.members)
             w, _ = pkg.pf_weights(ll, strict=False)
-            counts.append(int((w > 1.0 / a.members).sum()))
+            # w_i > 1/N_e, with equal weights (subset size 0) counted as the spec's N_e
+            counts.append(int((w >= (1.0 / a.members) * (1.0 - 1e-12)).sum()))
             if k == 0:
                 break
         print(f"{k},{np.mean(counts):.2f}")
