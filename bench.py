@@ -322,7 +322,7 @@ def main():
     backend = os.environ.get("DC_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or (os.environ.get("DC_BENCH_FORCE_SPLIT") == "1" and "RANK" in os.environ):
         import torch.distributed as dist
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -345,14 +345,18 @@ def main():
         cz_local = torch.zeros((M, 2), dtype=torch.float64, device=f"cuda:{local}")
         cz_all = torch.zeros((total, 2), dtype=torch.float64, device=f"cuda:{local}")
 
+        split = world > 1 or os.environ.get("DC_BENCH_FORCE_SPLIT") == "1"
+
         def cycle(c):
             obs = obs_all[c]
-            if world == 1:
+            if not split:
                 ens.da_cycle(5, obs, S, usig, c)
             else:
                 ens.da_cycle(5, np.zeros((0, 4)), S, usig, c)  # forecast + drifters only
                 ens.iewpf_begin(obs, S, usig, c, total, cz_ptr=cz_local.data_ptr())
-                if backend == "nccl":
+                if dist is None:  # single process forced through the split path
+                    cz_all.copy_(cz_local)
+                elif backend == "nccl":
                     dist.all_gather_into_tensor(cz_all, cz_local)
                 else:  # host-staged test path
                     host = cz_local.cpu()
