@@ -241,3 +241,39 @@ def test_one_stage_iewpf_bitwise(oracle):
     assert np.array_equal(wb, owb) and wb[0] == diag[:, 0].max() and wb[1] == 0.0
     assert np.array_equal(diag, od)
     assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
+
+
+def test_da_cycle_full_size_bitwise(oracle):
+    """One DA cycle at the bench size (500x300, 64 drifters on the bench lattice, drifter
+    copies in every member) for 3 members: state, drifters and diagnostics bitwise equal
+    to the oracle."""
+    pkg, cfg, p = setup(500, 300)
+    n = 3
+    e, u, v = spread_states(oracle, p, n, 23)
+    lx, ly = p.nx * p.dx, p.ny * p.dy
+    X, Y = np.meshgrid((np.arange(8) + 0.5) / 8 * lx, (np.arange(8) + 0.5) / 8 * ly)
+    lat = np.stack([X.ravel(), Y.ravel()], 1)
+    obs = np.hstack([lat + 1234.5, np.random.default_rng(29).normal(0, 20.0, (64, 2))])
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    pos = np.repeat(lat[None], n, 0).copy()
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    ens.drifters_set(pos)
+    ens.da_cycle(5, obs, S, usig, cycle=4)
+    ge, gu, gv, gt = ens.download()
+    gp, _ = ens.drifters_get()
+    diag, wb = ens.iewpf_diagnostics()
+    oe, ou, ov = e.copy(), u.copy(), v.copy()
+    op = pos.copy()
+    for m in range(n):
+        s = State(oe[m], ou[m], ov[m], 0.0)
+        for i in range(5):
+            oracle.advect_drifters(p, s, op[m], 60.0)
+            oracle.model_step(p, s, 1)
+            if i < 4:
+                oracle.perturb_philox(p, s, m, i)
+    od, owb = oracle.iewpf_assimilate(p, oe, ou, ov, obs, S, usig, 4)
+    assert np.array_equal(wb, owb) and np.array_equal(diag, od)
+    assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
+    assert np.array_equal(gp, op) and np.all(gt == 300.0)
