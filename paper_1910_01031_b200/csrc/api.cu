@@ -430,6 +430,12 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         choose_strips(ctx->sp, sms, swe_stage_occupancy());
     }
+    // CTA rows of the stage grid (members x strips, plus two tail strips per member) must
+    // fit gridDim.y
+    if (static_cast<long long>(ctx->M) * (ctx->sp.strips + 2) > 65535)
+        return set_err(ctx, DC_EINVAL,
+                       "too many members for one context (members x strips > 65535): split "
+                       "them over several contexts / GPUs");
     {
         const char* tr = std::getenv("DC_TAIL_ROWS");
         const char* ts = std::getenv("DC_TAIL_STRIPS");
