@@ -277,3 +277,34 @@ def test_da_cycle_full_size_bitwise(oracle):
     assert np.array_equal(wb, owb) and np.array_equal(diag, od)
     assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
     assert np.array_equal(gp, op) and np.all(gt == 300.0)
+
+
+@pytest.mark.parametrize("nx,ny,c", [(60, 60, 3), (110, 55, 5), (64, 48, 1), (125, 75, 5)])
+def test_da_cycle_configs_bitwise(oracle, nx, ny, c):
+    """DA cycles on other grids and coarsening factors (odd sizes, non-square, c_omega 1/3/5):
+    bitwise vs the oracle, two cycles so the second starts from an analysed state."""
+    pkg = _gpu()
+    cfg = pkg.Config(nx=nx, ny=ny, c_omega=c)
+    p = make_params(nx=nx, ny=ny, q0=cfg.q0, seed=cfg.seed, c_omega=c)
+    n = 3
+    e, u, v = spread_states(oracle, p, n, 31)
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    rng = np.random.default_rng(nx + ny + c)
+    obs = [np.hstack([rng.uniform(0, 1, (5, 2)) * [p.nx * p.dx, p.ny * p.dy],
+                      rng.normal(0, 20.0, (5, 2))]) for _ in range(2)]
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    for cyc in range(2):
+        ens.da_cycle(5, obs[cyc], S, usig, cycle=cyc)
+    ge, gu, gv, _ = ens.download()
+    oe, ou, ov = e.copy(), u.copy(), v.copy()
+    for cyc in range(2):
+        for m in range(n):
+            s = State(oe[m], ou[m], ov[m], 0.0)
+            for i in range(5):
+                oracle.model_step(p, s, 1)
+                if i < 4:
+                    oracle.perturb_philox(p, s, m, 4 * cyc + i)
+        oracle.iewpf_assimilate(p, oe, ou, ov, obs[cyc], S, usig, cyc)
+    assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
