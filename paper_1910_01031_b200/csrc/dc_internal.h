@@ -1,6 +1,7 @@
 // dc_internal.h -- private structures shared by the CUDA translation units and the
 // C-ABI implementation (api.cu). Not part of the public boundary.
 #pragma once
+#include <atomic>
 
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -60,6 +61,20 @@ struct ErrParams {
     double w[25];         // SOAR weights w[(db+2)*5 + (da+2)] (stochastic.hpp:54-57)
     double h_eq;
 };
+
+// Opt a kernel in to `bytes` of dynamic shared memory on the current device, once per
+// (kernel, device): the attribute is per device, so a process driving several GPUs needs
+// it on each of them.
+template <class F>
+inline void smem_opt_in(F* func, size_t bytes) {
+    static std::atomic<unsigned long long> done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_relaxed) & bit) return;
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    done.fetch_or(bit);
+}
 
 // stochastic.cu launchers
 void launch_philox_noise(cudaStream_t s, const ErrParams& ep, int M, uint64_t seed, uint64_t tag,

@@ -654,12 +654,7 @@ void launch_local_blocks(cudaStream_t s, const ErrParams& ep, const double* xi, 
     const size_t nr = static_cast<size_t>(ep.nxc) * ep.nyc;
     const size_t full = (49 * 49 + nr) * sizeof(double);
     const int in_smem = full <= 160 * 1024;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(local_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             160 * 1024);
-        attr = true;
-    }
+    smem_opt_in(local_blocks_kernel, 160 * 1024);
     local_blocks_kernel<<<M, 64 * kLbGroups, in_smem ? full : 49 * 49 * sizeof(double), s>>>(
         ep, xi, nu, scal, wb, cells, n_obs, order, level_start, n_levels, foffs, usig, z, err,
         in_smem, one_stage);

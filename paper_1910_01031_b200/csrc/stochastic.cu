@@ -270,12 +270,7 @@ void launch_philox_soar(cudaStream_t s, const ErrParams& ep, int M, uint64_t see
                         int64_t member_base, uint32_t substream, uint64_t draw, double* corr,
                         int* offsets, const int* err) {
     const size_t bytes = static_cast<size_t>(kBand + 4) * ep.nxc * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(philox_soar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        attr = true;
-    }
+    smem_opt_in(philox_soar_kernel, 200 * 1024);
     philox_soar_kernel<<<dim3((ep.nyc + kBand - 1) / kBand, M), 256, bytes, s>>>(
         ep, M, seed, tag, member_base, substream, draw, corr, offsets, err);
 }
