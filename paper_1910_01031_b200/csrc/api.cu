@@ -64,6 +64,24 @@ namespace dcg {
 __global__ void count_iters_kernel(const int* sub, int M, unsigned long long* acc);
 }
 
+// Every entry point that takes a context runs on that context's device (a process may
+// drive several GPUs, one context each) and restores the caller's current device.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const dc_ctx* c) {
+        int cur = 0;
+        if (c && cudaGetDevice(&cur) == cudaSuccess && cur != c->device) {
+            prev = cur;
+            cudaSetDevice(c->device);
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 namespace {
 
 const char* kVersion = "driftcast-b200 0.1 (sm_100a)";
@@ -370,7 +388,10 @@ dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base
     ctx->use_graph = !(ng && ng[0] == '1');
     derive_params(ctx);
     *out = ctx;
+    int prev_dev = -1;
+    cudaGetDevice(&prev_dev);
     dc_status st = dc_create_device(ctx, device, stream);
+    if (prev_dev >= 0 && prev_dev != device) cudaSetDevice(prev_dev);  // caller's device
     if (st) {
         std::fprintf(stderr, "dc_create: %s\n", ctx->err.c_str());
         dc_destroy(ctx);
@@ -511,6 +532,7 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
 }
 
 dc_status dc_destroy(dc_ctx* ctx) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return DC_OK;
     cudaStreamSynchronize(ctx->stream);
     if (ctx->step_exec) cudaGraphExecDestroy(ctx->step_exec);
@@ -535,6 +557,7 @@ dc_status dc_sync(dc_ctx* ctx) { return surface_errors(ctx); }
 
 const char* dc_last_error(dc_ctx* ctx, int32_t* member, int32_t* j, int32_t* k,
                           int32_t* substep) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return "null context";
     if (member) *member = ctx->em;
     if (j) *j = ctx->ej;
@@ -545,6 +568,7 @@ const char* dc_last_error(dc_ctx* ctx, int32_t* member, int32_t* j, int32_t* k,
 
 dc_status dc_upload_member(dc_ctx* ctx, int32_t m, const float* eta, const float* hu,
                            const float* hv, double t) {
+    DeviceGuard dg_(ctx);
     dc_status st = check_member(ctx, m);
     if (st) return st;
     const size_t off = static_cast<size_t>(m) * ctx->sp.ny * ctx->sp.pitch;
@@ -561,6 +585,7 @@ dc_status dc_upload_member(dc_ctx* ctx, int32_t m, const float* eta, const float
 
 dc_status dc_upload_all(dc_ctx* ctx, const float* eta, const float* hu, const float* hv,
                         const double* t) {
+    DeviceGuard dg_(ctx);
     const float* src[3] = {eta, hu, hv};
     for (int i = 0; i < 3; ++i)
         CU(cudaMemcpy2DAsync(ctx->f[i], ctx->sp.pitch * sizeof(float), src[i],
@@ -576,6 +601,7 @@ dc_status dc_upload_all(dc_ctx* ctx, const float* eta, const float* hu, const fl
 
 dc_status dc_download_member(dc_ctx* ctx, int32_t m, float* eta, float* hu, float* hv,
                              double* t) {
+    DeviceGuard dg_(ctx);
     dc_status st = check_member(ctx, m);
     if (st) return st;
     st = surface_errors(ctx);
@@ -594,6 +620,7 @@ dc_status dc_download_member(dc_ctx* ctx, int32_t m, float* eta, float* hu, floa
 }
 
 dc_status dc_download_all(dc_ctx* ctx, float* eta, float* hu, float* hv, double* t) {
+    DeviceGuard dg_(ctx);
     dc_status st = surface_errors(ctx);
     float* dst[3] = {eta, hu, hv};
     for (int i = 0; i < 3; ++i)
@@ -612,6 +639,7 @@ dc_status dc_download_all(dc_ctx* ctx, float* eta, float* hu, float* hv, double*
 // init_double_jet (swe.hpp:459-500): fp64 profile on the host (same libm as the
 // reference build), broadcast to every member, t = 0.
 dc_status dc_init_double_jet(dc_ctx* ctx) {
+    DeviceGuard dg_(ctx);
     const dc_config& g = ctx->cfg;
     const int nx = g.nx, ny = g.ny;
     const double ly = ny * g.dy;
@@ -650,6 +678,7 @@ dc_status dc_init_double_jet(dc_ctx* ctx) {
 }
 
 dc_status dc_step(dc_ctx* ctx, int32_t n_steps) {
+    DeviceGuard dg_(ctx);
     if (n_steps < 0) return set_err(ctx, DC_EINVAL, "dc_step: n_steps < 0");
     if (ctx->use_graph && !ctx->step_exec) {
         dc_status st = build_step_graph(ctx, true, &ctx->step_exec);
@@ -686,12 +715,14 @@ dc_status dc_step(dc_ctx* ctx, int32_t n_steps) {
 }
 
 dc_status dc_substeps(dc_ctx* ctx, int32_t* out) {
+    DeviceGuard dg_(ctx);
     CU(cudaMemcpyAsync(out, ctx->ctl.sub, ctx->M * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return DC_OK;
 }
 
 dc_status dc_flux_rhs(dc_ctx* ctx, int32_t m, float* d_eta, float* d_hu, float* d_hv) {
+    DeviceGuard dg_(ctx);
     dc_status st = check_member(ctx, m);
     if (st) return st;
     const size_t per = static_cast<size_t>(ctx->sp.ny) * ctx->sp.pitch;
@@ -727,6 +758,7 @@ dc_status dc_flux_rhs(dc_ctx* ctx, int32_t m, float* d_eta, float* d_hu, float* 
 }
 
 dc_status dc_cfl_dt(dc_ctx* ctx, double* dt_out) {
+    DeviceGuard dg_(ctx);
     const int M = ctx->M;
     CU(cudaMemsetAsync(ctx->gmax, 0, 2 * M * sizeof(unsigned long long), ctx->stream));
     std::vector<int> big(M, 0x7fffffff);
@@ -760,6 +792,7 @@ dc_status dc_cfl_dt(dc_ctx* ctx, double* dt_out) {
 }
 
 dc_status dc_perturb(dc_ctx* ctx, int32_t mode, const int32_t* offsets, const double* xi) {
+    DeviceGuard dg_(ctx);
     if (ctx->cfg.q0 == 0.0) return DC_OK; // stochastic.hpp:167: consumes no randomness
     const int M = ctx->M;
     if (mode == DC_NOISE_PHILOX) {
@@ -795,6 +828,7 @@ dc_status dc_perturb(dc_ctx* ctx, int32_t mode, const int32_t* offsets, const do
 }
 
 dc_status dc_add_q_half(dc_ctx* ctx, const int32_t* offsets, const double* coarse, double scale) {
+    DeviceGuard dg_(ctx);
     const int M = ctx->M;
     for (int m = 0; m < 2 * M; ++m)
         if (offsets[m] < 0 || offsets[m] >= ctx->cfg.c_omega)
@@ -811,6 +845,7 @@ dc_status dc_add_q_half(dc_ctx* ctx, const int32_t* offsets, const double* coars
 }
 
 dc_status dc_get_config(dc_ctx* ctx, dc_config* cfg, int32_t* n_members, int64_t* member_base) {
+    DeviceGuard dg_(ctx);
     if (!ctx) return DC_ESTATE;
     if (cfg) *cfg = ctx->cfg;
     if (n_members) *n_members = ctx->M;
@@ -819,11 +854,13 @@ dc_status dc_get_config(dc_ctx* ctx, dc_config* cfg, int32_t* n_members, int64_t
 }
 
 dc_status dc_get_draw_counter(dc_ctx* ctx, uint64_t* d) {
+    DeviceGuard dg_(ctx);
     *d = ctx->me_draw;
     return DC_OK;
 }
 
 dc_status dc_set_model_error_tag(dc_ctx* ctx, uint64_t tag) {
+    DeviceGuard dg_(ctx);
     if (tag != 1 && tag != 3)
         return set_err(ctx, DC_EINVAL, "model-error stream tag must be model_error (1) or "
                                        "truth_model_error (3)");
@@ -832,11 +869,13 @@ dc_status dc_set_model_error_tag(dc_ctx* ctx, uint64_t tag) {
 }
 
 dc_status dc_set_draw_counter(dc_ctx* ctx, uint64_t d) {
+    DeviceGuard dg_(ctx);
     ctx->me_draw = d;
     return DC_OK;
 }
 
 int64_t dc_kernel_launches(dc_ctx* ctx) {
+    DeviceGuard dg_(ctx);
     // graph path: 2 kernels per step + 3 per substep iteration (counted on the device)
     unsigned long long iters = 0;
     if (ctx->use_graph && ctx->substep_iters) {
@@ -850,6 +889,7 @@ int64_t dc_kernel_launches(dc_ctx* ctx) {
 void* dc_stream(dc_ctx* ctx) { return ctx->stream; }
 
 dc_status dc_counters(dc_ctx* ctx, uint64_t* out) {
+    DeviceGuard dg_(ctx);
     unsigned long long g[2] = {0, 0}, h[2] = {0, 0};
     CU(cudaMemcpyAsync(g, ctx->substep_iters, sizeof(g), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaMemcpyAsync(h, ctx->host_iters, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
@@ -861,6 +901,7 @@ dc_status dc_counters(dc_ctx* ctx, uint64_t* out) {
 }
 
 dc_status dc_time_stages(dc_ctx* ctx, int32_t n_substeps, double* ms_out) {
+    DeviceGuard dg_(ctx);
     // One model step's worth of substeps launched individually with CUDA events around
     // each stage kernel on the context stream (advances the state like dc_step). All
     // launches and events are queued back to back and read after one synchronisation,
