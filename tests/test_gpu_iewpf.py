@@ -308,3 +308,31 @@ def test_da_cycle_configs_bitwise(oracle, nx, ny, c):
                     oracle.perturb_philox(p, s, m, 4 * cyc + i)
         oracle.iewpf_assimilate(p, oe, ou, ov, obs[cyc], S, usig, cyc)
     assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
+
+
+def test_twenty_cycles_bitwise(oracle):
+    """A long horizon: 20 DA cycles (100 model steps, 80 model-error draws, 20 analyses)
+    stay bitwise equal to the oracle -- no drift accumulates anywhere on the path."""
+    pkg, cfg, p = setup()
+    n = 3
+    e, u, v = spread_states(oracle, p, n, 41)
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    rng = np.random.default_rng(43)
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    oe, ou, ov = e.copy(), u.copy(), v.copy()
+    for cyc in range(20):
+        obs = np.hstack([rng.uniform(0, 1, (4, 2)) * [p.nx * p.dx, p.ny * p.dy],
+                         rng.normal(0, 20.0, (4, 2))])
+        ens.da_cycle(5, obs, S, usig, cycle=cyc)
+        for m in range(n):
+            s = State(oe[m], ou[m], ov[m], 0.0)
+            for i in range(5):
+                oracle.model_step(p, s, 1)
+                if i < 4:
+                    oracle.perturb_philox(p, s, m, 4 * cyc + i)
+        oracle.iewpf_assimilate(p, oe, ou, ov, obs, S, usig, cyc)
+    ge, gu, gv, gt = ens.download()
+    assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
+    assert np.all(gt == 20 * 300.0)
