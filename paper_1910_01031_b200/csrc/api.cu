@@ -51,6 +51,8 @@ struct dc_ctx {
     bool use_graph = true;
     int64_t launches = 0;
     int last_max_sub = 8;
+    // substep end fused into stage 2 (DC_FUSED_END=0: the separate substep_end launch)
+    bool fused_end = true;
     // CTA row units of the SWE stage grid (big strips first, short ones last)
     int2* units = nullptr;
     // IEWPF / observation / drifter state
@@ -242,7 +244,6 @@ dc_status build_step_graph(dc_ctx* ctx, bool with_scan, cudaGraphExec_t* exec) {
         launch_reset_stats(s, ctx->sp, ctx->ctl);
         launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
     }
-    launch_step_begin(s, ctx->sp, ctx->ctl);
     cudaStreamCaptureStatus st;
     cudaGraph_t cap = nullptr;
     const cudaGraphNode_t* deps = nullptr;
@@ -250,6 +251,9 @@ dc_status build_step_graph(dc_ctx* ctx, bool with_scan, cudaGraphExec_t* exec) {
     CU(cudaStreamGetCaptureInfo(s, &st, nullptr, &cap, &deps, &ndeps));
     cudaGraphConditionalHandle handle;
     CU(cudaGraphConditionalHandleCreate(&handle, cap, 1, cudaGraphCondAssignDefault));
+    const unsigned long long h = static_cast<unsigned long long>(handle);
+    launch_step_begin(s, ctx->sp, ctx->ctl, h, ctx->fused_end ? 1 : 0);
+    CU(cudaStreamGetCaptureInfo(s, &st, nullptr, &cap, &deps, &ndeps));
     cudaGraphNodeParams cp{};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = handle;
@@ -265,8 +269,9 @@ dc_status build_step_graph(dc_ctx* ctx, bool with_scan, cudaGraphExec_t* exec) {
     launch_stage(bs, ctx->sp, ctx->exact, 1, ctx->f[0], ctx->f[1], ctx->f[2], nullptr, nullptr,
                  nullptr, ctx->f[3], ctx->f[4], ctx->f[5], ctx->ctl);
     launch_stage(bs, ctx->sp, ctx->exact, 2, ctx->f[3], ctx->f[4], ctx->f[5], ctx->f[0],
-                 ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
-    launch_substep_end(bs, ctx->sp, ctx->ctl, static_cast<unsigned long long>(handle), 1);
+                 ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl, h,
+                 ctx->fused_end ? 2 : 0);
+    if (!ctx->fused_end) launch_substep_end(bs, ctx->sp, ctx->ctl, h, 1);
     cudaGraph_t body_out = nullptr;
     CU(cudaStreamEndCapture(bs, &body_out));
     CU(cudaStreamDestroy(bs));
@@ -295,9 +300,13 @@ dc_status step_host_loop(dc_ctx* ctx, bool with_scan) {
             launch_stage(s, ctx->sp, ctx->exact, 1, ctx->f[0], ctx->f[1], ctx->f[2], nullptr,
                          nullptr, nullptr, ctx->f[3], ctx->f[4], ctx->f[5], ctx->ctl);
             launch_stage(s, ctx->sp, ctx->exact, 2, ctx->f[3], ctx->f[4], ctx->f[5], ctx->f[0],
-                         ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
-            launch_substep_end(s, ctx->sp, ctx->ctl, 0ull, 0);
-            ctx->launches += 3;
+                         ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl, 0ull,
+                         ctx->fused_end ? 1 : 0);
+            ctx->launches += 2;
+            if (!ctx->fused_end) {
+                launch_substep_end(s, ctx->sp, ctx->ctl, 0ull, 0);
+                ctx->launches += 1;
+            }
         }
         done += guess;
         int any = 0;
@@ -386,6 +395,8 @@ dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base
     ctx->exact = cfg->exact_fp != 0;
     const char* ng = std::getenv("DC_NO_GRAPH");
     ctx->use_graph = !(ng && ng[0] == '1');
+    const char* fe = std::getenv("DC_FUSED_END");
+    ctx->fused_end = !(fe && fe[0] == '0');
     derive_params(ctx);
     *out = ctx;
     int prev_dev = -1;
@@ -484,8 +495,8 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
         CU(cudaMemsetAsync(ctx->f[i], 0, ctx->field_elems * sizeof(float), ctx->stream));
     }
     const int M = ctx->M;
-    // 11 arrays, each rounded up to 16 bytes by take()
-    size_t bytes = 11 * ((static_cast<size_t>(M) * 4 * sizeof(double) + 15) / 16 * 16) + 64;
+    // 13 arrays, each rounded up to 16 bytes by take()
+    size_t bytes = 13 * ((static_cast<size_t>(M) * 4 * sizeof(double) + 15) / 16 * 16) + 64;
     CU(cudaMalloc(&ctx->ctl_mem, bytes));
     CU(cudaMemsetAsync(ctx->ctl_mem, 0, bytes, ctx->stream));
     char* p = static_cast<char*>(ctx->ctl_mem);
@@ -505,6 +516,8 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     ctx->ctl.err_sub = reinterpret_cast<int*>(take(M * sizeof(int)));
     ctx->ctl.mx = reinterpret_cast<unsigned*>(take(4 * M * sizeof(unsigned)));
     ctx->ctl.any_active = reinterpret_cast<int*>(take(sizeof(int)));
+    ctx->ctl.n_active = reinterpret_cast<int*>(take(sizeof(int)));
+    ctx->ctl.mdone = reinterpret_cast<unsigned*>(take(M * sizeof(unsigned)));
     CU(cudaMalloc(&ctx->substep_iters, 2 * sizeof(unsigned long long)));
     CU(cudaMalloc(&ctx->host_iters, 2 * sizeof(unsigned long long)));
     CU(cudaMemsetAsync(ctx->host_iters, 0, 2 * sizeof(unsigned long long), ctx->stream));
@@ -876,14 +889,15 @@ dc_status dc_set_draw_counter(dc_ctx* ctx, uint64_t d) {
 
 int64_t dc_kernel_launches(dc_ctx* ctx) {
     DeviceGuard dg_(ctx);
-    // graph path: 2 kernels per step + 3 per substep iteration (counted on the device)
+    // graph path: 2 kernels per step + 2 per substep iteration (3 with the separate
+    // substep_end), iterations counted on the device
     unsigned long long iters = 0;
     if (ctx->use_graph && ctx->substep_iters) {
         cudaMemcpyAsync(&iters, ctx->substep_iters, sizeof(iters), cudaMemcpyDeviceToHost,
                         ctx->stream);
         cudaStreamSynchronize(ctx->stream);
     }
-    return ctx->launches + 3 * static_cast<int64_t>(iters);
+    return ctx->launches + (ctx->fused_end ? 2 : 3) * static_cast<int64_t>(iters);
 }
 
 void* dc_stream(dc_ctx* ctx) { return ctx->stream; }

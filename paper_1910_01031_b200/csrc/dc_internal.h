@@ -32,6 +32,9 @@ struct SweParams {
     int by, strips;       // rows per CTA strip, strips per member (uniform strips)
     const int2* units;    // optional CTA row units {m, y0 | y1 << 16}: big strips first,
     int n_units;          // short ones last so the final wave drains quickly (api.cu)
+    int ctas_per_member;  // stage-2 CTAs of one member (set per launch by launch_stage)
+    int end_mode;         // stage 2: fused substep end (0 off, 1 flag only, 2 + graph cond)
+    unsigned long long end_cond;  // cudaGraphConditionalHandle of the step's while node
     float H, g, theta, cf_x, cf_y, inv_g, idx, idy, fH;
     double dx, dy, courant, model_dt, h_eq, gd;
     float neg_zero;       // -0.0f, opaque to ptxas (packed-product addend, swe.cu)
@@ -50,6 +53,8 @@ struct StepCtl {
     int* err_sub;       // substep index of a non-finite failure
     unsigned* mx;       // [M][4]: max|u|+c bits, max|v|+c bits, ordered min h, spare
     int* any_active;    // loop condition (host-visible in the fallback path)
+    unsigned* mdone;    // [M] stage-2 CTAs of the member finished this substep (fused end)
+    int* n_active;      // members still stepping (fused end: the last one ends the loop)
 };
 
 struct ErrParams {
@@ -95,12 +100,18 @@ void launch_q_half_apply(cudaStream_t s, const SweParams& sp, const ErrParams& e
 // swe.cu launchers
 void launch_cfl_scan(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
                      const float* hv, StepCtl ctl);
-void launch_step_begin(cudaStream_t s, const SweParams& sp, StepCtl ctl);
+void launch_step_begin(cudaStream_t s, const SweParams& sp, StepCtl ctl,
+                       unsigned long long cond_handle = 0, int use_cond = 0);
 void launch_reset_stats(cudaStream_t s, const SweParams& sp, StepCtl ctl);
 int swe_stage_occupancy();
+// end_mode of a stage-2 launch: 0 = a separate launch_substep_end follows; 1 = each
+// member's last stage-2 CTA runs the member's substep end (loop flag read by the host);
+// 2 = same, and the CTA that retires the last active member clears the graph's while
+// condition (cond_handle)
 void launch_stage(cudaStream_t s, const SweParams& sp, bool exact, int stage, const float* ie,
                   const float* iu, const float* iv, const float* s0e, const float* s0u,
-                  const float* s0v, float* oe, float* ou, float* ov, StepCtl ctl);
+                  const float* s0v, float* oe, float* ou, float* ov, StepCtl ctl,
+                  unsigned long long cond_handle = 0, int end_mode = 0);
 void launch_substep_end(cudaStream_t s, const SweParams& sp, StepCtl ctl,
                         unsigned long long cond_handle, int use_cond);
 void launch_selftest_math(cudaStream_t s, unsigned long long* counts);
