@@ -28,6 +28,8 @@ KEYS = {
     "launch__grid_size": "grid",
     "launch__block_size": "block",
     "launch__occupancy_limit_registers": "ctas_per_sm_by_regs",
+    "sm__cycles_active.avg": "sm_active_cycles",
+    "gpc__cycles_elapsed.max": "elapsed_cycles",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0,
          "msecond": 1e3}
@@ -64,6 +66,9 @@ def rep_rows(rep):
                     continue
                 if v >= 0.05:
                     st[k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = round(v, 3)
+        if rec.get("sm_active_cycles") and rec.get("elapsed_cycles"):
+            # share of the launch the SMs had resident CTAs (ramp + drain = the rest)
+            rec["sm_active_frac"] = round(rec["sm_active_cycles"] / rec["elapsed_cycles"], 4)
         rec["stalls_per_issue"] = dict(sorted(st.items(), key=lambda x: -x[1]))
         out.append(rec)
     return out
