@@ -430,6 +430,13 @@ static void choose_strips(SweParams& P, int sms, int per_sm) {
             P.strips = strips;
         }
     }
+    if (const char* sr = std::getenv("DC_STRIP_ROWS")) {  // fixed strip height (experiments)
+        const int by = std::atoi(sr);
+        if (by >= 4 && by <= P.ny) {
+            P.by = by;
+            P.strips = (P.ny + by - 1) / by;
+        }
+    }
 }
 
 // Row units {m, y0 | y1 << 16} of the stage grid: every member's rows as big strips (the

@@ -107,6 +107,45 @@ def test_model_step_bitwise_10_members(oracle):
     ens.close()
 
 
+def _step_vs_oracle(oracle, nx, ny, n, steps, seed):
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair(nx, ny)
+    e, u, v = perturbed_jets(oracle, p, n, seed=seed)
+    ens = Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    ens.model_step(steps)
+    ge, gu, gv, gt = ens.download()
+    subs = ens.substeps()
+    ens.close()
+    for m in range(n):
+        s = State(e[m].copy(), u[m].copy(), v[m].copy(), 0.0)
+        dts = oracle.model_step(p, s, steps)
+        assert np.array_equal(ge[m], s.eta), (nx, ny, m, np.abs(ge[m] - s.eta).max())
+        assert np.array_equal(gu[m], s.hu), (nx, ny, m)
+        assert np.array_equal(gv[m], s.hv), (nx, ny, m)
+        assert gt[m] == s.t and subs[m] == len(dts)
+
+
+# column counts around the 252-column CTA tile (one tile exactly, one column into a
+# second tile, odd widths whose column pairs straddle the periodic seam), row counts
+# with and without the short tail strips, a single member
+@pytest.mark.parametrize("nx,ny,n", [(252, 40, 3), (253, 37, 2), (257, 64, 2), (101, 150, 3),
+                                     (504, 301, 2), (37, 23, 1)])
+def test_model_step_bitwise_shapes(oracle, nx, ny, n):
+    _step_vs_oracle(oracle, nx, ny, n, 2, seed=nx + ny)
+
+
+# launch-shape knobs read at context creation: strip heights, tail strips, the separate
+# substep_end launch, the host-driven substep loop -- all must give the same bits
+@pytest.mark.parametrize("env", [{"DC_TAIL_ROWS": "0"}, {"DC_TAIL_ROWS": "7", "DC_TAIL_STRIPS": "3"},
+                                 {"DC_STRIP_ROWS": "13"}, {"DC_FUSED_END": "0"},
+                                 {"DC_NO_GRAPH": "1"}, {"DC_NO_GRAPH": "1", "DC_FUSED_END": "0"}])
+def test_model_step_bitwise_launch_variants(oracle, monkeypatch, env):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _step_vs_oracle(oracle, 500, 300, 3, 2, seed=11)
+
+
 def test_model_step_fma_tolerance(oracle):
     """FMA build (exact_fp=0): the stencil contracts to FFMA, so the trajectory drifts
     from the reference at round-off level. Stated tolerance: max|diff| <= 5e-5 of
