@@ -397,8 +397,40 @@ def main():
 
         # ---- end to end through the C ABI with host buffers ----
         diag_bytes = M * 40 + 16
-        drift_bytes = M * len(drift0) * 2 * (8 + 4)
+        n_d = len(drift0)
+        drift_bytes = M * n_d * 2 * (8 + 4)
         obs_bytes = obs_all.shape[1] * 32
+        # forecast statistics against the truth drifters: one rank holds
+        # every member's drifters after an all-gather in member-id order
+        truth_ok = args.obs == "drifters" and obs_all.shape[1] == n_d
+        fe_bytes = 16 * n_d + 16 if truth_ok and rank == 0 else 0
+        if truth_ok and dist is not None:
+            dev = f"cuda:{local}"
+            lpos = torch.empty((M, n_d, 2), dtype=torch.float64, device=dev)
+            lwind = torch.empty((M, n_d, 2), dtype=torch.int32, device=dev)
+            gpos = torch.empty((total, n_d, 2), dtype=torch.float64, device=dev)
+            gwind = torch.empty((total, n_d, 2), dtype=torch.int32, device=dev)
+
+        def forecast_stats(c):
+            truth = obs_all[c][:, :2]
+            if dist is None:
+                return ens.forecast_error(truth)
+            ens.drifters_to_device(lpos.data_ptr(), lwind.data_ptr())
+            if backend == "nccl":
+                dist.all_gather_into_tensor(gpos, lpos)
+                dist.all_gather_into_tensor(gwind, lwind)
+            else:  # host-staged test path
+                for src, dst in ((lpos, gpos), (lwind, gwind)):
+                    host = src.cpu()
+                    parts = [torch.zeros_like(host) for _ in range(world)]
+                    dist.all_gather(parts, host)
+                    dst.copy_(torch.cat(parts))
+            if rank == 0:
+                return pkg.forecast_error_gathered(cfg, total, n_d, gpos.data_ptr(),
+                                                   gwind.data_ptr(), truth, device=local,
+                                                   stream=stream.cuda_stream)
+            return None
+
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
@@ -406,6 +438,8 @@ def main():
         for c in range(W + K, W + 2 * K):
             cycle(c)
             ens.iewpf_diagnostics()    # D2H per-particle (c, phi, gamma, zeta, alpha) + (w, beta)
+            if truth_ok:
+                forecast_stats(c)      # E(t), RMSE(t) of the drifter forecast (D2H 16 B/drifter)
             ens.drifters_get()         # D2H forecast drifter ensemble
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
@@ -471,7 +505,8 @@ def main():
         "cycle_ms": ms / K,
         "cell_model_steps_per_s": value / max(1.0, cell_updates / (K * 5 * total * cfg.nx * cfg.ny)),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": obs_bytes,
-                "d2h_bytes_per_step": diag_bytes + drift_bytes, "ms_per_step": wall * 1e3 / K},
+                "d2h_bytes_per_step": diag_bytes + drift_bytes + fe_bytes,
+                "ms_per_step": wall * 1e3 / K},
         "gpu_launches": int(l1 - l0),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,

@@ -208,6 +208,17 @@ dc_status dc_resample_members(dc_ctx* ctx, const int32_t* idx);
  * positions. Ed / Rd ([n_d]) may be NULL. Synchronous. */
 dc_status dc_forecast_error(dc_ctx* ctx, const double* truth_xy, double* E, double* RMSE,
                             double* Ed, double* Rd);
+/* Multi-GPU forecast statistics: each rank copies its drifter ensemble
+ * into device buffers ([n_members][n_d][2] fp64 positions, int32 winding counts) with
+ * dc_drifters_get_device (stream-ordered on the context stream), the ranks gather them
+ * in member-id order (NCCL), and one rank evaluates forecast_error over all members with
+ * dc_forecast_error_gathered on `stream` of `device` -- bitwise equal to dc_forecast_error
+ * of one context holding every member. Both synchronous on return of the statistics. */
+dc_status dc_drifters_get_device(dc_ctx* ctx, double* d_pos, int32_t* d_wind);
+dc_status dc_forecast_error_gathered(const dc_config* cfg, int32_t device, void* stream,
+                                     int32_t n_members, int32_t n_d, const double* d_pos,
+                                     const int32_t* d_wind, const double* truth_xy, double* E,
+                                     double* RMSE, double* Ed, double* Rd);
 /* Observation file: UTF-8 lines "time,kind,id,x,y,y_hu,y_hv" with kind
  * "drifter" | "mooring" and %.17g numbers (exact round trip). read: *n_out = records in
  * the file; recs may be NULL to count; DC_EINVAL if capacity is too small. Host only. */

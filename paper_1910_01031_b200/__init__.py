@@ -5,10 +5,10 @@ CUDA kernels behind the C ABI in include/driftcast_gpu.h.
 The compute lives in libdriftcast_gpu.so (C++/CUDA). This package only binds it.
 """
 from ._lib import DcError, load  # noqa: F401
-from .ensemble import (Config, Ensemble, generate_truth, obs_array, pf_weights,  # noqa: F401
-                       precompute_S, precompute_local_svd, read_obs_file, residual_resample,
+from .ensemble import (Config, Ensemble, forecast_error_gathered, generate_truth,  # noqa: F401
+                       obs_array, pf_weights, precompute_S, precompute_local_svd, read_obs_file, residual_resample,
                        write_obs_file)
 
 __all__ = ["Config", "Ensemble", "DcError", "load", "obs_array", "precompute_S",
            "precompute_local_svd", "pf_weights", "residual_resample", "write_obs_file",
-           "read_obs_file", "generate_truth"]
+           "read_obs_file", "generate_truth", "forecast_error_gathered"]

@@ -78,7 +78,7 @@ EXPORTS = [
     "dc_pf_loglik", "dc_pf_weights", "dc_residual_resample", "dc_resample_members",
     "dc_forecast_error", "dc_obs_file_write", "dc_obs_file_read", "dc_trajectory_write",
     "dc_set_model_error_tag", "dc_generate_truth", "dc_iewpf_set_mode",
-    "dc_iewpf_diagnostics_write",
+    "dc_iewpf_diagnostics_write", "dc_drifters_get_device", "dc_forecast_error_gathered",
 ]
 
 
@@ -157,6 +157,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "dc_residual_resample": (st, [dp, C.c_int32, C.c_uint64, C.c_uint64, ip]),
         "dc_resample_members": (st, [vp, ip]),
         "dc_forecast_error": (st, [vp, dp, dp, dp, dp, dp]),
+        "dc_drifters_get_device": (st, [vp, vp, vp]),
+        "dc_forecast_error_gathered": (st, [cfgp, C.c_int32, vp, C.c_int32, C.c_int32, vp, vp,
+                                            dp, dp, dp, dp, dp]),
         "dc_obs_file_write": (st, [C.c_char_p, C.POINTER(DcObsRecord), C.c_int32, C.c_int32]),
         "dc_obs_file_read": (st, [C.c_char_p, C.POINTER(DcObsRecord), C.c_int32, ip]),
         "dc_trajectory_write": (st, [vp, C.c_char_p, C.c_double, C.c_int32]),

@@ -286,6 +286,11 @@ class Ensemble:
         self._ck(self.L.dc_forecast_error(self.h, _d(t), C.byref(E), C.byref(R), _d(ed), _d(rd)))
         return E.value, R.value, ed, rd
 
+    def drifters_to_device(self, pos_ptr, wind_ptr):
+        """Stream-ordered copy of the drifter ensemble into device buffers
+        ([n][n_d][2] fp64 / int32), e.g. torch tensors feeding an NCCL gather."""
+        self._ck(self.L.dc_drifters_get_device(self.h, C.c_void_p(pos_ptr), C.c_void_p(wind_ptr)))
+
     def trajectory_write(self, path, time, append=True):
         self._ck(self.L.dc_trajectory_write(self.h, str(path).encode(), time, int(append)))
 
@@ -340,6 +345,27 @@ class Ensemble:
         S = np.ascontiguousarray(S, np.float64).reshape(4)
         usig = np.ascontiguousarray(usig, np.float64).reshape(49 * 49)
         self._ck(self.L.dc_da_cycle(self.h, n_steps, arr, n, _d(S), _d(usig), cycle))
+
+
+def forecast_error_gathered(cfg: Config, n_members, n_drifters, pos_ptr, wind_ptr, truth_xy,
+                            device=0, stream=None):
+    """forecast_error over drifter ensembles gathered (member-id order) into device memory
+    from several ranks: returns (E, RMSE, E_d, RMSE_d) like Ensemble.forecast_error."""
+    L = _lib.load()
+    c = cfg.to_c()
+    t = np.ascontiguousarray(truth_xy, np.float64).reshape(-1, 2)
+    if t.shape[0] != n_drifters:
+        raise ValueError("truth_xy must hold one position per drifter")
+    E, R = C.c_double(0), C.c_double(0)
+    ed = np.empty(n_drifters, np.float64)
+    rd = np.empty(n_drifters, np.float64)
+    rc = L.dc_forecast_error_gathered(C.byref(c), device, C.c_void_p(stream) if stream else None,
+                                      n_members, n_drifters, C.c_void_p(pos_ptr),
+                                      C.c_void_p(wind_ptr), _d(t), C.byref(E), C.byref(R),
+                                      _d(ed), _d(rd))
+    if rc:
+        raise DcError(rc, "dc_forecast_error_gathered failed")
+    return E.value, R.value, ed, rd
 
 
 def precompute_S(cfg: Config, r_hu=1.0, r_hv=1.0):

@@ -114,6 +114,46 @@ def test_forecast_error_matches_oracle(oracle):
     assert E == Eo and R == Ro and np.array_equal(ed, edo) and np.array_equal(rd, rdo)
 
 
+def test_forecast_error_gathered_slices_equal_one_context(oracle):
+    """ranks hold member slices; their drifter ensembles gathered into one
+    device buffer (member-id order) give forecast statistics bitwise equal to one context
+    holding every member (two contexts on one GPU stand in for two ranks)."""
+    import torch
+    pkg, cfg, p = setup()
+    n, cut = 7, 3
+    e, u, v = spread_states(oracle, p, n, 5)
+    rng = np.random.default_rng(21)
+    pos = rng.uniform(0, 1, (6, 2)) * [p.nx * p.dx, p.ny * p.dy]
+    whole = pkg.Ensemble(cfg, n)
+    parts = [pkg.Ensemble(cfg, cut), pkg.Ensemble(cfg, n - cut, member_base=cut)]
+    whole.upload(e, u, v, 0.0)
+    parts[0].upload(e[:cut], u[:cut], v[:cut], 0.0)
+    parts[1].upload(e[cut:], u[cut:], v[cut:], 0.0)
+    for ens in [whole] + parts:
+        ens.drifters_set(pos)
+        for _ in range(3):
+            ens.advect_drifters(60.0)
+            ens.model_step(1)
+            ens.perturb_state()
+    truth = (pos + rng.normal(0, 2000.0, pos.shape)) % [p.nx * p.dx, p.ny * p.dy]
+    gpos = torch.empty((n, 6, 2), dtype=torch.float64, device="cuda")
+    gwind = torch.empty((n, 6, 2), dtype=torch.int32, device="cuda")
+    parts[0].drifters_to_device(gpos[:cut].data_ptr(), gwind[:cut].data_ptr())
+    parts[1].drifters_to_device(gpos[cut:].data_ptr(), gwind[cut:].data_ptr())
+    for ens in parts:
+        ens.sync()
+    E, R, ed, rd = pkg.forecast_error_gathered(cfg, n, 6, gpos.data_ptr(), gwind.data_ptr(),
+                                               truth)
+    Ew, Rw, edw, rdw = whole.forecast_error(truth)
+    assert E == Ew and R == Rw and np.array_equal(ed, edw) and np.array_equal(rd, rdw)
+    wp, ww = whole.drifters_get()
+    assert np.array_equal(gpos.cpu().numpy(), wp) and np.array_equal(gwind.cpu().numpy(), ww)
+    with pytest.raises(pkg.DcError):
+        pkg.forecast_error_gathered(cfg, n, 6, 0, 0, truth)
+    for ens in [whole] + parts:
+        ens.close()
+
+
 def test_snapshot_bytes_match_reference_writer(oracle, ref, tmp_path):
     pkg, cfg, p = setup()
     e, u, v = spread_states(oracle, p, 2, 4)
