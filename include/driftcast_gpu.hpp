@@ -185,6 +185,10 @@ public:
         check(dc_forecast_error(ctx_, truth_xy.data(), &e, &r, nullptr, nullptr));
         return {e, r};
     }
+    // multi-GPU forecast statistics: this rank's drifters into device buffers for a gather
+    void drifters_to_device(double* d_pos, std::int32_t* d_wind) {
+        check(dc_drifters_get_device(ctx_, d_pos, d_wind));
+    }
 
     void sync() { check(dc_sync(ctx_)); }
 
@@ -196,6 +200,21 @@ private:
     int n_;
     dc_ctx* ctx_ = nullptr;
 };
+
+// forecast_error over drifter ensembles gathered from every rank (member-id order, device
+// buffers): {E, RMSE}, bitwise equal to one context holding every member
+inline std::pair<double, double> forecast_error_gathered(const dc_config& cfg, int device,
+                                                         void* stream, int n_members, int n_d,
+                                                         const double* d_pos,
+                                                         const std::int32_t* d_wind,
+                                                         const std::vector<double>& truth_xy) {
+    double e = 0.0, r = 0.0;
+    const dc_status st = dc_forecast_error_gathered(&cfg, device, stream, n_members, n_d, d_pos,
+                                                    d_wind, truth_xy.data(), &e, &r, nullptr,
+                                                    nullptr);
+    if (st) throw_status(st, "dc_forecast_error_gathered failed");
+    return {e, r};
+}
 
 } // namespace gpu
 } // namespace driftcast
