@@ -138,11 +138,16 @@ class Ensemble:
         eta, hu, hv = (np.ascontiguousarray(a, np.float32) for a in (eta, hu, hv))
         self._ck(self.L.dc_upload_member(self.h, m, _f(eta), _f(hu), _f(hv), t))
 
-    def download(self):
+    def download(self, strict=True):
+        """All members' fields and times. A member that failed (dry cell, non-finite
+        state, runaway substeps) raises DcError unless strict=False, which returns every
+        member's fields as they are -- the failed ones stopped where they failed."""
         shp = (self.n, self.cfg.ny, self.cfg.nx)
         e, u, v = (np.empty(shp, np.float32) for _ in range(3))
         t = np.empty(self.n, np.float64)
-        self._ck(self.L.dc_download_all(self.h, _f(e), _f(u), _f(v), _d(t)))
+        rc = self.L.dc_download_all(self.h, _f(e), _f(u), _f(v), _d(t))
+        if rc and (strict or rc not in (_lib.DC_EDRY, _lib.DC_ENONFINITE, _lib.DC_ERUNAWAY)):
+            self._ck(rc)
         return e, u, v, t
 
     def download_member(self, m):

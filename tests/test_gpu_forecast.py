@@ -319,3 +319,40 @@ def test_non_finite_state_reported_like_reference(oracle, ref, field, value):
     assert eg.value.status == 3 and eg.value.member == 1
     assert er.value.msg in eg.value.message, (er.value.msg, eg.value.message)
     assert eg.value.message.startswith("model_step: non-finite value after substep ")
+
+
+# every substep-loop variant must retire errored members and finish the step: a member
+# dry at step start (never steps), one poisoned mid-substep (non-finite), all members dry
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("env", [{}, {"DC_FUSED_END": "0"}, {"DC_NO_GRAPH": "1"},
+                                 {"DC_NO_GRAPH": "1", "DC_FUSED_END": "0"}])
+def test_errored_members_retire_in_every_loop_variant(oracle, monkeypatch, env):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, Ensemble = _gpu()
+    from paper_1910_01031_b200 import DcError
+    cfg, p = cfg_pair(100, 60)
+    e, u, v = perturbed_jets(oracle, p, 4, seed=6)
+    e[1, 10, 20] = -231.0  # dry at step start
+    u[2, 30, 40] = np.nan  # non-finite after the first substep
+    ens = Ensemble(cfg, 4)
+    ens.upload(e, u, v, 0.0)
+    with pytest.raises(DcError):
+        ens.model_step(2)
+        ens.sync()
+    with pytest.raises(DcError):
+        ens.download()
+    ge, gu, gv, gt = ens.download(strict=False)
+    for m in (0, 3):  # the healthy members stepped on, bitwise
+        s = State(e[m].copy(), u[m].copy(), v[m].copy(), 0.0)
+        oracle.model_step(p, s, 2)
+        assert np.array_equal(ge[m], s.eta) and np.array_equal(gu[m], s.hu)
+        assert np.array_equal(gv[m], s.hv) and gt[m] == s.t
+    ens.close()
+    e[:, 10, 20] = -231.0  # nobody can step
+    ens = Ensemble(cfg, 4)
+    ens.upload(e, u, v, 0.0)
+    with pytest.raises(DcError):
+        ens.model_step(1)
+        ens.sync()
+    ens.close()
