@@ -213,7 +213,8 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
     __shared__ tile::Smem S;
     __shared__ float ST[3][TY][TX];  // the tile's state across all observations
     const int m = blockIdx.y;
-    if (err[m]) return;
+    // another tile of the member may raise E_DRY_ADD meanwhile: decide once per CTA
+    if (__syncthreads_or(err[m] != 0)) return;
     const int tl = blockIdx.x;
     const int cnt = counts[tl];
     if (cnt == 0) return;

@@ -158,7 +158,8 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
     __shared__ float ST[3][TY][TX];
     __shared__ float red[3][8];
     const int m = blockIdx.z;
-    if (err[m]) return;
+    // another tile of the member may raise E_DRY_ADD meanwhile: decide once per CTA
+    if (__syncthreads_or(err[m] != 0)) return;
     const int j0 = blockIdx.x * TX, k0 = blockIdx.y * TY;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int j = j0 + tx;
