@@ -514,7 +514,11 @@ def main():
                      "stage_ms": [ms1, ms2], "peak_source": peak_src,
                      "note": "the stage kernel is FP32-pipe bound, not HBM bound (DESIGN.md "
                              "§4): see fp32 for the binding roofline",
-                     "fp32": fp32_roofline(ms1, ms2, cells, clocks)},
+                     "fp32": fp32_roofline(ms1, ms2, cells, clocks),
+                     # the 24 B/cell-update lower bound of a single-sweep
+                     # substep (read psi, write psi), at the same substep time
+                     "single_sweep_24B": {"achieved": 24.0 * cells / ((ms1 + ms2) / 1e3) / 1e9,
+                                          "frac": 24.0 * cells / ((ms1 + ms2) / 1e3) / 1e9 / peak}},
         "cpu_baseline": cpu,
         "clocks": clocks,
     }
