@@ -212,6 +212,16 @@ def profiled_traffic():
         return None
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_sample(cfg_params, obs, n_members, threads, base_state):
     """The reference's CPU forecast (Stepper::model_step + perturb_state, threaded) for a
     bounded member sample + the restated analysis on that sample. Returns
@@ -290,10 +300,10 @@ def run_reference(args, rank, world):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 state / f64 covariance", "data": "synthetic",
-        "config": {"workload": "configs[1]: double jet 500x300, IEWPF cycle (5 model steps, "
-                               "4 model-error draws, 64 drifter obs)",
-                   "members_sampled": sample, "nx": p.nx, "ny": p.ny},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": kind,
+        "config": {"workload": workload_name(args, args.members),
+                   "cycle": "5 x 60 s steps, model error after 4, IEWPF analysis",
+                   "members_sampled": sample, "nx": p.nx, "ny": p.ny, "obs": args.obs},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": kind, "cpu": cpu_model(),
                          "sample": f"{sample} members x 1 IEWPF cycle per step (forecast via "
                                    f"the reference operators, analysis via the CPU "
                                    f"restatement; both on {threads} threads)"},
@@ -473,7 +483,7 @@ def main():
             sample = max(2, min(threads, 16))
             base = Oracle().init_double_jet(p)
             dt, cu, kind = cpu_reference_sample(p, obs_all[0], sample, threads, base)
-            cpu = {"value": cu / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            cpu = {"value": cu / dt, "unit": UNIT, "cores": threads, "kind": kind, "cpu": cpu_model(),
                    "sample": f"{sample} members x 1 IEWPF cycle (5 model steps, 4 perturbs, "
                              f"{obs_all.shape[1]} obs): forecast on the reference operators "
                              f"over {threads} threads, analysis via the CPU restatement"}
