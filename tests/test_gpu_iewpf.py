@@ -135,6 +135,35 @@ def test_iewpf_assimilate_bitwise(oracle, nx, ny, n, n_obs):
     assert np.all((diag[:, 4] > 0) & (diag[:, 4] <= 1.0 + 1e-12))
 
 
+def test_iewpf_edge_observations_bitwise(oracle):
+    """Observations on the domain edges (x = 0, y = 0, just below Lx / Ly), exactly on
+    cell faces and coarse-cell corners, and two observations at the same point: cell
+    location, window alignment across the periodic seam and the sequential pulls all
+    match the oracle bit for bit."""
+    pkg, cfg, p = setup(100, 60)
+    lx, ly = p.nx * p.dx, p.ny * p.dy
+    rng = np.random.default_rng(17)
+    xy = np.array([[0.0, 0.0], [np.nextafter(lx, 0.0), 3.0 * p.dy],
+                   [7.0 * p.dx, np.nextafter(ly, 0.0)], [5.0 * p.c_omega * p.dx, 10.0 * p.c_omega * p.dy],
+                   [40.0 * p.dx, 20.0 * p.dy], [40.0 * p.dx, 20.0 * p.dy],
+                   [0.5 * lx, 0.5 * ly]])
+    obs = np.hstack([xy, rng.normal(0, 20.0, (len(xy), 2))])
+    n = 4
+    e, u, v = spread_states(oracle, p, n, 13)
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    ens.iewpf_assimilate(obs, S, usig, cycle=5)
+    ge, gu, gv, _ = ens.download()
+    diag, wb = ens.iewpf_diagnostics()
+    ens.close()
+    oe, ou, ov = e.copy(), u.copy(), v.copy()
+    od, owb = oracle.iewpf_assimilate(p, oe, ou, ov, obs, S, usig, 5)
+    assert np.array_equal(wb, owb) and np.array_equal(diag, od)
+    assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
+
+
 def test_iewpf_two_slices_equal_one(oracle):
     """The multi-GPU decomposition on one device: two contexts own members [0,3) and
     [3,6); stages 1-3 run per slice, the (c, zeta) pairs are concatenated (the NCCL
