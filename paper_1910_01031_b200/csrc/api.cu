@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -57,6 +59,7 @@ struct dc_ctx {
     int2* units = nullptr;
     // IEWPF / observation / drifter state
     IewpfBuffers iw{};
+    FeScratch fe{};  // forecast_error scratch
     // error reporting
     std::string err;
     int em = -1, ej = -1, ek = -1, esub = -1;
@@ -568,6 +571,7 @@ dc_status dc_destroy(dc_ctx* ctx) {
     cudaFree(ctx->gmax);
     cudaFree(ctx->rhs);
     iewpf_free(ctx->iw);
+    fe_free(ctx->fe);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return DC_OK;

@@ -33,8 +33,13 @@ struct IewpfBuffers {
     double S_host[4] = {0, 0, 0, 0};
     std::vector<double> usig_host;
     bool usig_valid = false;
-    void* stage = nullptr;    // pinned host staging
-    size_t stage_bytes = 0;
+    // pinned host staging ring for observation uploads: a slot is reused only after the
+    // event recorded behind its H2D copy completed, so an upload never drains the stream
+    static constexpr int kStageSlots = 4;
+    unsigned char* stage = nullptr;  // kStageSlots x stage_bytes
+    size_t stage_bytes = 0;          // per slot
+    cudaEvent_t stage_ev[kStageSlots] = {nullptr, nullptr, nullptr, nullptr};
+    int stage_next = 0;
     // local-block schedule: observation ids ordered by dependency level
     int* lb_order = nullptr;  // [cap_obs]
     int* lb_start = nullptr;  // [cap_obs + 1] first position of each level in lb_order
@@ -47,6 +52,22 @@ struct IewpfBuffers {
     int* dwind = nullptr;     // [M][n_d][2]
 };
 
+// persistent scratch of forecast_error (per-drifter E_d, RMSE_d): device truth and results,
+// pinned host copies; grown on demand, never freed per call
+struct FeScratch {
+    int cap = 0;
+    double* d_truth = nullptr;  // [cap][2]
+    double* d_out = nullptr;    // [2][cap] E_d, RMSE_d
+    double* h_io = nullptr;     // pinned [4][cap]: truth in, E_d / RMSE_d out
+};
+
+inline void fe_free(FeScratch& f) {
+    if (f.d_truth) cudaFree(f.d_truth);
+    if (f.d_out) cudaFree(f.d_out);
+    if (f.h_io) cudaFreeHost(f.h_io);
+    f = FeScratch{};
+}
+
 inline void iewpf_free(IewpfBuffers& b) {
     void* ps[] = {b.obs, b.cells, b.d, b.sd, b.win, b.tile_lists, b.tile_count, b.nu, b.scal,
                   b.cz, b.cz_all, b.wb, b.S, b.usig, b.foffs, b.dpos, b.dwind, b.z, b.bad,
@@ -54,6 +75,8 @@ inline void iewpf_free(IewpfBuffers& b) {
     for (void* p : ps)
         if (p) cudaFree(p);
     if (b.stage) cudaFreeHost(b.stage);
+    for (cudaEvent_t e : b.stage_ev)
+        if (e) cudaEventDestroy(e);
     b = IewpfBuffers{};
 }
 
