@@ -121,37 +121,74 @@ __global__ void resample_members_kernel(int M, int n_d, const int* __restrict__ 
     }
 }
 
-// one thread per drifter: E_d = mean_i |x_i - truth|^2 and the ensemble mean of the
+// one CTA per drifter: E_d = mean_i |x_i - truth|^2 and the ensemble mean of the
 // unwrapped positions (x + wind * L), then RMSE_d = mean_i |x_i - mean|^2, distances by
-// the minimal periodic image, members in id order
-__global__ void forecast_error_kernel(SweParams sp, int M, int n_d, const double* __restrict__ pos,
-                                      const int* __restrict__ wind,
-                                      const double* __restrict__ truth, double* ed, double* rd) {
-    const int d = blockIdx.x * blockDim.x + threadIdx.x;
-    if (d >= n_d) return;
+// the minimal periodic image. The per-member terms are computed in parallel, a chunk of
+// kFeThreads members at a time; thread 0 folds each chunk in member-id order, so the sums
+// are the sequential ones (bitwise equal to the oracle and to any member partition).
+constexpr int kFeThreads = 128;
+
+__global__ void __launch_bounds__(kFeThreads)
+forecast_error_kernel(SweParams sp, int M, int n_d, const double* __restrict__ pos,
+                      const int* __restrict__ wind, const double* __restrict__ truth,
+                      double* ed, double* rd) {
+    __shared__ double t_e[kFeThreads], t_x[kFeThreads], t_y[kFeThreads];
+    __shared__ double s_mean[2];
+    const int d = blockIdx.x;
+    const int t = threadIdx.x;
     const double lx = sp.nx * sp.dx, ly = sp.ny * sp.dy;
     const double tx = truth[2 * d], ty = truth[2 * d + 1];
     double se = 0.0, sx = 0.0, sy = 0.0;
-    for (int m = 0; m < M; ++m) {
-        const size_t q = (static_cast<size_t>(m) * n_d + d) * 2;
-        const double ex = min_image(pos[q] - tx, lx), ey = min_image(pos[q + 1] - ty, ly);
-        se = se + (ex * ex + ey * ey);
-        sx = sx + (pos[q] + wind[q] * lx);
-        sy = sy + (pos[q + 1] + wind[q + 1] * ly);
+    for (int m0 = 0; m0 < M; m0 += kFeThreads) {
+        const int m = m0 + t;
+        if (m < M) {
+            const size_t q = (static_cast<size_t>(m) * n_d + d) * 2;
+            const double ex = min_image(pos[q] - tx, lx), ey = min_image(pos[q + 1] - ty, ly);
+            t_e[t] = ex * ex + ey * ey;
+            t_x[t] = pos[q] + wind[q] * lx;
+            t_y[t] = pos[q + 1] + wind[q + 1] * ly;
+        }
+        __syncthreads();
+        if (t == 0) {
+            const int n = min(kFeThreads, M - m0);
+            for (int i = 0; i < n; ++i) {
+                se = se + t_e[i];
+                sx = sx + t_x[i];
+                sy = sy + t_y[i];
+            }
+        }
+        __syncthreads();
     }
-    const double mx = sx / M, my = sy / M;
-    // wrap the mean into the domain for the minimal-image spread
-    double wx = fmod(mx, lx), wy = fmod(my, ly);
-    if (wx < 0.0) wx += lx;
-    if (wy < 0.0) wy += ly;
+    if (t == 0) {
+        const double mx = sx / M, my = sy / M;
+        // wrap the mean into the domain for the minimal-image spread
+        double wx = fmod(mx, lx), wy = fmod(my, ly);
+        if (wx < 0.0) wx += lx;
+        if (wy < 0.0) wy += ly;
+        s_mean[0] = wx;
+        s_mean[1] = wy;
+    }
+    __syncthreads();
+    const double wx = s_mean[0], wy = s_mean[1];
     double sr = 0.0;
-    for (int m = 0; m < M; ++m) {
-        const size_t q = (static_cast<size_t>(m) * n_d + d) * 2;
-        const double ex = min_image(pos[q] - wx, lx), ey = min_image(pos[q + 1] - wy, ly);
-        sr = sr + (ex * ex + ey * ey);
+    for (int m0 = 0; m0 < M; m0 += kFeThreads) {
+        const int m = m0 + t;
+        if (m < M) {
+            const size_t q = (static_cast<size_t>(m) * n_d + d) * 2;
+            const double ex = min_image(pos[q] - wx, lx), ey = min_image(pos[q + 1] - wy, ly);
+            t_e[t] = ex * ex + ey * ey;
+        }
+        __syncthreads();
+        if (t == 0) {
+            const int n = min(kFeThreads, M - m0);
+            for (int i = 0; i < n; ++i) sr = sr + t_e[i];
+        }
+        __syncthreads();
     }
-    ed[d] = se / M;
-    rd[d] = sr / M;
+    if (t == 0) {
+        ed[d] = se / M;
+        rd[d] = sr / M;
+    }
 }
 
 } // namespace
@@ -186,7 +223,7 @@ void launch_resample(cudaStream_t s, const SweParams& sp, int M, const int* idx,
 
 void launch_forecast_error(cudaStream_t s, const SweParams& sp, int M, int n_d, const double* pos,
                            const int* wind, const double* truth, double* ed, double* rd) {
-    forecast_error_kernel<<<(n_d + 63) / 64, 64, 0, s>>>(sp, M, n_d, pos, wind, truth, ed, rd);
+    forecast_error_kernel<<<n_d, kFeThreads, 0, s>>>(sp, M, n_d, pos, wind, truth, ed, rd);
 }
 
 } // namespace dcg

@@ -114,6 +114,26 @@ def test_forecast_error_matches_oracle(oracle):
     assert E == Eo and R == Ro and np.array_equal(ed, edo) and np.array_equal(rd, rdo)
 
 
+def test_forecast_error_many_members_matches_oracle(oracle):
+    """More members than one chunk of the per-drifter CTA (128): the chunked member-order
+    folds still give the sequential sums bit for bit."""
+    pkg, cfg, p = setup()
+    n, n_d = 300, 5
+    rng = np.random.default_rng(17)
+    lx, ly = p.nx * p.dx, p.ny * p.dy
+    ens = pkg.Ensemble(cfg, n)
+    ens.init_double_jet()
+    ens.drifters_set(rng.uniform(0, 1, (n, n_d, 2)) * [lx, ly])
+    for _ in range(40):  # the jet carries drifters across the periodic edge: windings
+        ens.advect_drifters(3000.0)
+    gp, gw = ens.drifters_get()
+    assert np.any(gw != 0)
+    truth = rng.uniform(0, 1, (n_d, 2)) * [lx, ly]
+    E, R, ed, rd = ens.forecast_error(truth)
+    Eo, Ro, edo, rdo = oracle.forecast_error(p, gp, gw, truth)
+    assert E == Eo and R == Ro and np.array_equal(ed, edo) and np.array_equal(rd, rdo)
+
+
 def test_forecast_error_gathered_slices_equal_one_context(oracle):
     """ranks hold member slices; their drifter ensembles gathered into one
     device buffer (member-id order) give forecast statistics bitwise equal to one context
