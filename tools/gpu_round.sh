@@ -11,6 +11,8 @@ python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "sm
 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"; tail -c 600 $O/bench.json
 python bench.py --obs moorings --no-cpu-baseline > $O/bench_moorings.json 2> $O/bench_moorings.err; echo "moorings rc=$?"
 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc=$?"
+python bench.py --nx 1000 --ny 600 --members 125 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench_configs4.json 2> $O/bench_configs4.err; echo "configs4 rc=$?"
+python tools/e2e_probe.py --cycles 10 > $O/e2e_probe.log 2>&1; echo "e2e probe rc=$?"
 export DC_NO_GRAPH=1
 if python tools/profile_cycle.py --cycles 2 > $O/profile_cycle.log 2>&1; then
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \

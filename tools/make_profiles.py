@@ -82,6 +82,8 @@ def main(tag):
                          f"tools/profile_cycle.py --cycles 2 (100 members, 500x300, 64 drifters); "
                          f"serialised cold-cache launches", "total_us": round(tot, 1),
                "kernels": sh}, open(os.path.join(prof, "r1_launches_cycle.json"), "w"), indent=1)
+    import shutil
+    shutil.copy(os.path.join(g, f"launches_{tag}.csv"), os.path.join(prof, "r1_launches_cycle.csv"))
     groups = {"swe": "r1_swe_stage_ncu.json", "q_half_apply": "r1_perturb_ncu.json",
               "pull_apply": "r1_analysis_ncu.json", "local_blocks": "r1_local_blocks_ncu.json",
               "philox_soar": "r1_philox_soar_ncu.json", "cfl_scan": "r1_cfl_scan_ncu.json"}
