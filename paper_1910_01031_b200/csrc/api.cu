@@ -57,6 +57,9 @@ struct dc_ctx {
     bool fused_end = true;
     // CTA row units of the SWE stage grid (big strips first, short ones last)
     int2* units = nullptr;
+    // persistent model step (DC_PERSISTENT): grid and row strips per member
+    bool persist = false;
+    int p_grid = 0, p_nsp = 1;
     // IEWPF / observation / drifter state
     IewpfBuffers iw{};
     FeScratch fe{};  // forecast_error scratch
@@ -471,6 +474,14 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         choose_strips(ctx->sp, sms, swe_stage_occupancy());
+        const char* pe = std::getenv("DC_PERSISTENT");
+        ctx->persist = pe && std::atoi(pe) != 0;
+        if (ctx->persist) {
+            ctx->p_grid = sms * swe_persistent_occupancy();
+            const char* pr = std::getenv("DC_PSTRIP_ROWS");
+            const int rows = std::max(4, pr ? std::atoi(pr) : 75);
+            ctx->p_nsp = std::max(1, std::min(ctx->sp.ny / 4, (ctx->sp.ny + rows / 2) / rows));
+        }
     }
     // CTA rows of the stage grid (members x strips, plus two tail strips per member) must
     // fit gridDim.y
@@ -505,8 +516,8 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
         CU(cudaMemsetAsync(ctx->f[i], 0, ctx->field_elems * sizeof(float), ctx->stream));
     }
     const int M = ctx->M;
-    // 13 arrays, each rounded up to 16 bytes by take()
-    size_t bytes = 13 * ((static_cast<size_t>(M) * 4 * sizeof(double) + 15) / 16 * 16) + 64;
+    // 17 arrays, each rounded up to 16 bytes by take()
+    size_t bytes = 17 * ((static_cast<size_t>(M) * 4 * sizeof(double) + 15) / 16 * 16) + 64;
     CU(cudaMalloc(&ctx->ctl_mem, bytes));
     CU(cudaMemsetAsync(ctx->ctl_mem, 0, bytes, ctx->stream));
     char* p = static_cast<char*>(ctx->ctl_mem);
@@ -528,6 +539,10 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     ctx->ctl.any_active = reinterpret_cast<int*>(take(sizeof(int)));
     ctx->ctl.n_active = reinterpret_cast<int*>(take(sizeof(int)));
     ctx->ctl.mdone = reinterpret_cast<unsigned*>(take(M * sizeof(unsigned)));
+    ctx->ctl.next = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long)));
+    ctx->ctl.s1c = reinterpret_cast<unsigned*>(take(M * sizeof(unsigned)));
+    ctx->ctl.dsub = reinterpret_cast<int*>(take(M * sizeof(int)));
+    ctx->ctl.hang = reinterpret_cast<int*>(take(sizeof(int)));
     CU(cudaMalloc(&ctx->substep_iters, 2 * sizeof(unsigned long long)));
     CU(cudaMalloc(&ctx->host_iters, 2 * sizeof(unsigned long long)));
     CU(cudaMemsetAsync(ctx->host_iters, 0, 2 * sizeof(unsigned long long), ctx->stream));
@@ -723,7 +738,19 @@ dc_status dc_step(dc_ctx* ctx, int32_t n_steps) {
     }
     for (int i = 0; i < n_steps; ++i) {
         const bool scan = ctx->stats != 1;
-        if (ctx->use_graph) {
+        if (ctx->persist) {
+            if (scan) {
+                launch_reset_stats(ctx->stream, ctx->sp, ctx->ctl);
+                launch_cfl_scan(ctx->stream, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+            }
+            launch_step_begin(ctx->stream, ctx->sp, ctx->ctl, 0ull, 0);
+            launch_step_persistent(ctx->stream, ctx->sp, ctx->exact, ctx->p_grid, ctx->p_nsp,
+                                   ctx->f[0], ctx->f[1], ctx->f[2], ctx->f[3], ctx->f[4],
+                                   ctx->f[5], ctx->ctl);
+            dcg::count_iters_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->ctl.sub, ctx->M,
+                                                                ctx->substep_iters);
+            ctx->launches += (scan ? 2 : 0) + 3;
+        } else if (ctx->use_graph) {
             CU(cudaGraphLaunch(scan ? ctx->step_exec : ctx->step_exec_fused, ctx->stream));
             dcg::count_iters_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->ctl.sub, ctx->M,
                                                                 ctx->substep_iters);

@@ -55,6 +55,11 @@ struct StepCtl {
     int* any_active;    // loop condition (host-visible in the fallback path)
     unsigned* mdone;    // [M] stage-2 CTAs of the member finished this substep (fused end)
     int* n_active;      // members still stepping (fused end: the last one ends the loop)
+    // persistent step (DC_PERSISTENT): work-unit counter and per-member progress
+    unsigned long long* next;  // next work unit to claim
+    unsigned* s1c;      // [M] stage-1 units completed this step (all substeps)
+    int* dsub;          // [M] substep ends published this step (release / acquire)
+    int* hang;          // a dependency wait timed out (scheduling bug guard)
 };
 
 struct ErrParams {
@@ -108,6 +113,10 @@ int swe_stage_occupancy();
 // member's last stage-2 CTA runs the member's substep end (loop flag read by the host);
 // 2 = same, and the CTA that retires the last active member clears the graph's while
 // condition (cond_handle)
+int launch_step_persistent(cudaStream_t s, const SweParams& sp, bool exact, int grid, int nsp,
+                          float* fe, float* fu, float* fv, float* ge, float* gu, float* gv,
+                          StepCtl ctl);
+int swe_persistent_occupancy();
 void launch_stage(cudaStream_t s, const SweParams& sp, bool exact, int stage, const float* ie,
                   const float* iu, const float* iv, const float* s0e, const float* s0u,
                   const float* s0v, float* oe, float* ou, float* ov, StepCtl ctl,

@@ -136,10 +136,13 @@ def test_model_step_bitwise_shapes(oracle, nx, ny, n):
 
 
 # launch-shape knobs read at context creation: strip heights, tail strips, the separate
-# substep_end launch, the host-driven substep loop -- all must give the same bits
+# substep_end launch, the host-driven substep loop, the persistent one-launch step (with
+# several strip heights) -- all must give the same bits
 @pytest.mark.parametrize("env", [{"DC_TAIL_ROWS": "0"}, {"DC_TAIL_ROWS": "7", "DC_TAIL_STRIPS": "3"},
                                  {"DC_STRIP_ROWS": "13"}, {"DC_FUSED_END": "0"},
-                                 {"DC_NO_GRAPH": "1"}, {"DC_NO_GRAPH": "1", "DC_FUSED_END": "0"}])
+                                 {"DC_NO_GRAPH": "1"}, {"DC_NO_GRAPH": "1", "DC_FUSED_END": "0"},
+                                 {"DC_PERSISTENT": "1"},
+                                 {"DC_PERSISTENT": "1", "DC_PSTRIP_ROWS": "7"}])
 def test_model_step_bitwise_launch_variants(oracle, monkeypatch, env):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -325,7 +328,8 @@ def test_non_finite_state_reported_like_reference(oracle, ref, field, value):
 # dry at step start (never steps), one poisoned mid-substep (non-finite), all members dry
 @pytest.mark.timeout(300)
 @pytest.mark.parametrize("env", [{}, {"DC_FUSED_END": "0"}, {"DC_NO_GRAPH": "1"},
-                                 {"DC_NO_GRAPH": "1", "DC_FUSED_END": "0"}])
+                                 {"DC_NO_GRAPH": "1", "DC_FUSED_END": "0"},
+                                 {"DC_PERSISTENT": "1"}])
 def test_errored_members_retire_in_every_loop_variant(oracle, monkeypatch, env):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
