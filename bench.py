@@ -10,8 +10,10 @@ observations every 5 min. One bench "step" = one full IEWPF cycle (SPEC.md:603-6
   value  = ensemble cell-updates/s (one cell of one member through one SSP-RK2
            substep), device-timed with CUDA events over K cycles, state resident in HBM
   e2e    = the same metric through the C ABI with host buffers: the cycle's observation
-           records copied host->device inside the call, and per-particle diagnostics +
-           drifter positions read back device->host every cycle, wall-clock timed
+           records (and the truth drifter positions) copied host->device inside the calls,
+           per-particle diagnostics, drifter positions and forecast statistics read back
+           device->host every cycle into pinned slots (cycle c read while c+1 runs),
+           wall-clock timed
   N > 1  = one process per GPU (torchrun), 100 members per rank (weak scaling); the
            only collective is the NCCL all-gather of (c_i, zeta_i) at the IEWPF barrier.
 
@@ -406,14 +408,16 @@ def main():
         value = cell_updates / (ms / 1e3)
 
         # ---- end to end through the C ABI with host buffers ----
-        diag_bytes = M * 40 + 16
+        # pipelined readback slots: err flags + the raw per-particle scalars + (w, beta)
+        diag_bytes = M * 4 + M * 8 * 8 + 16
         n_d = len(drift0)
         drift_bytes = M * n_d * 2 * (8 + 4)
         obs_bytes = obs_all.shape[1] * 32
         # forecast statistics against the truth drifters: one rank holds
         # every member's drifters after an all-gather in member-id order
         truth_ok = args.obs == "drifters" and obs_all.shape[1] == n_d
-        fe_bytes = 16 * n_d + 16 if truth_ok and rank == 0 else 0
+        fe_bytes = 16 * n_d if truth_ok and rank == 0 else 0  # E_d, RMSE_d per drifter
+        truth_bytes = 16 * n_d if truth_ok and rank == 0 else 0  # truth positions H2D
         if truth_ok and dist is not None:
             dev = f"cuda:{local}"
             lpos = torch.empty((M, n_d, 2), dtype=torch.float64, device=dev)
@@ -445,12 +449,20 @@ def main():
             dist.barrier()
         t0 = time.perf_counter()
         e2e_cu0 = ens.counters()[1]
-        for c in range(W + K, W + 2 * K):
+        # each cycle's outputs (per-particle diagnostics + (w, beta), the drifter forecast
+        # ensemble, E(t) / RMSE(t) against the truth drifters) go D2H into a pinned slot
+        # queued behind the cycle; the host reads cycle c while cycle c+1 runs
+        for i, c in enumerate(range(W + K, W + 2 * K)):
             cycle(c)
-            ens.iewpf_diagnostics()    # D2H per-particle (c, phi, gamma, zeta, alpha) + (w, beta)
-            if truth_ok:
-                forecast_stats(c)      # E(t), RMSE(t) of the drifter forecast (D2H 16 B/drifter)
-            ens.drifters_get()         # D2H forecast drifter ensemble
+            if truth_ok and dist is None:
+                ens.readback_enqueue(i % 2, truth_xy=obs_all[c][:, :2])
+            else:
+                ens.readback_enqueue(i % 2)
+                if truth_ok:
+                    forecast_stats(c)  # ranks gather drifters, rank 0 evaluates (synchronous)
+            if i > 0:
+                ens.readback_wait((i - 1) % 2)
+        ens.readback_wait((K - 1) % 2)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         e2e_cu = (ens.counters()[1] - e2e_cu0) * cfg.nx * cfg.ny
@@ -514,7 +526,7 @@ def main():
                          f"{6 * M * cfg.ny * ((cfg.nx + 31) // 32 * 32) * 4 / 1e6:.0f} MB vs 126 MB L2"},
         "cycle_ms": ms / K,
         "cell_model_steps_per_s": value / max(1.0, cell_updates / (K * 5 * total * cfg.nx * cfg.ny)),
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": obs_bytes,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": obs_bytes + truth_bytes,
                 "d2h_bytes_per_step": diag_bytes + drift_bytes + fe_bytes,
                 "ms_per_step": wall * 1e3 / K},
         "gpu_launches": int(l1 - l0),

@@ -281,6 +281,22 @@ dc_status dc_iewpf_diagnostics(dc_ctx* ctx, dc_particle_diag* per_member, double
 dc_status dc_iewpf_diagnostics_write(dc_ctx* ctx, const char* path, uint64_t cycle,
                                      int32_t append);
 
+/* ---- pipelined per-cycle readback ----------------------------------------------
+ * dc_readback_enqueue queues, behind the work already on the context stream, copies of
+ * the cycle's outputs into one of two pinned slots -- `what` = DC_READBACK_* bits: the
+ * particle diagnostics + (w_target, beta) of dc_iewpf_diagnostics, the drifter ensemble
+ * of dc_drifters_get, and forecast_error against truth_xy [n_d][2] (copied at the call) --
+ * and returns at once. dc_readback_wait(slot) blocks until that slot's copies landed and
+ * unpacks them (NULL outputs are skipped); values equal the synchronous calls' bit for
+ * bit. A driver enqueues cycle c, queues cycle c+1, then waits for c: the device never
+ * idles on the host. Device errors of the queued work surface at the wait. */
+#define DC_READBACK_DIAG 1
+#define DC_READBACK_DRIFTERS 2
+#define DC_READBACK_FORECAST_ERROR 4
+dc_status dc_readback_enqueue(dc_ctx* ctx, int32_t slot, int32_t what, const double* truth_xy);
+dc_status dc_readback_wait(dc_ctx* ctx, int32_t slot, dc_particle_diag* per_member,
+                           double* w_beta, double* pos, int32_t* wind, double* E, double* RMSE);
+
 /* ---- one data-assimilation cycle ----------------------------- */
 /* n_steps model steps; model error (PHILOX) after each but the last; drifters advected
  * by model_dt before each step when drifters are set; then the IEWPF analysis

@@ -63,6 +63,7 @@ struct dc_ctx {
     // IEWPF / observation / drifter state
     IewpfBuffers iw{};
     FeScratch fe{};  // forecast_error scratch
+    ReadbackSlot rb[kReadbackSlots];  // pipelined per-cycle outputs
     // error reporting
     std::string err;
     int em = -1, ej = -1, ek = -1, esub = -1;
@@ -587,6 +588,7 @@ dc_status dc_destroy(dc_ctx* ctx) {
     cudaFree(ctx->rhs);
     iewpf_free(ctx->iw);
     fe_free(ctx->fe);
+    readback_free(ctx->rb);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return DC_OK;

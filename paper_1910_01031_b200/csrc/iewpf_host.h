@@ -61,6 +61,26 @@ struct FeScratch {
     double* h_io = nullptr;     // pinned [4][cap]: truth in, E_d / RMSE_d out
 };
 
+// pinned readback slots (dc_readback_enqueue / dc_readback_wait): one cycle's outputs
+// copied device -> host behind the cycle's work, read by the host while later cycles run
+struct ReadbackSlot {
+    bool used = false;       // enqueued and not yet waited for
+    bool has_diag = false, has_drift = false, has_fe = false;
+    int n_d = 0;
+    size_t cap = 0;          // bytes of buf
+    unsigned char* buf = nullptr;  // pinned: err[M] | scal[M*8] | wb[2] | pos | wind | truth | fe
+    cudaEvent_t ev = nullptr;
+};
+constexpr int kReadbackSlots = 2;
+
+inline void readback_free(ReadbackSlot* r) {
+    for (int i = 0; i < kReadbackSlots; ++i) {
+        if (r[i].buf) cudaFreeHost(r[i].buf);
+        if (r[i].ev) cudaEventDestroy(r[i].ev);
+        r[i] = ReadbackSlot{};
+    }
+}
+
 inline void fe_free(FeScratch& f) {
     if (f.d_truth) cudaFree(f.d_truth);
     if (f.d_out) cudaFree(f.d_out);

@@ -340,6 +340,37 @@ class Ensemble:
         arr = np.array([[x.c, x.phi, x.gamma, x.zeta, x.alpha] for x in d], np.float64)
         return arr, wb
 
+    # ---- pipelined per-cycle readback (dc_readback_enqueue / dc_readback_wait) ----
+    def readback_enqueue(self, slot, diag=True, drifters=True, truth_xy=None):
+        """Queue copies of the outputs of the work queued so far into pinned slot 0 or 1
+        (particle diagnostics, drifter ensemble, forecast_error vs truth_xy); returns at
+        once. Read them with readback_wait(slot), e.g. after queueing the next cycle."""
+        what = (1 if diag else 0) | (2 if drifters else 0) | (4 if truth_xy is not None else 0)
+        t = None if truth_xy is None else np.ascontiguousarray(truth_xy, np.float64).reshape(-1, 2)
+        self._ck(self.L.dc_readback_enqueue(self.h, slot, what, None if t is None else _d(t)))
+        if not hasattr(self, "_rb_what"):
+            self._rb_what = {}
+        self._rb_what[slot] = what
+
+    def readback_wait(self, slot):
+        """Block until slot's copies landed; returns dict(diag [n,5] (c, phi, gamma, zeta,
+        alpha), w_beta, pos, wind, E, RMSE) with None for what was not queued."""
+        what = getattr(self, "_rb_what", {}).pop(slot, 0)
+        diag = np.empty((self.n, 5), np.float64) if what & 1 else None
+        wb = np.empty(2, np.float64) if what & 1 else None
+        pos = wind = None
+        if what & 2:
+            pos = np.empty((self.n, self.n_drifters, 2), np.float64)
+            wind = np.empty((self.n, self.n_drifters, 2), np.int32)
+        E, R = C.c_double(0), C.c_double(0)
+        self._ck(self.L.dc_readback_wait(
+            self.h, slot, None if diag is None else diag.ctypes.data_as(C.POINTER(DcParticleDiag)),
+            None if wb is None else _d(wb), None if pos is None else _d(pos),
+            None if wind is None else _i(wind), C.byref(E), C.byref(R)))
+        fe = bool(what & 4)
+        return {"diag": diag, "w_beta": wb, "pos": pos, "wind": wind,
+                "E": E.value if fe else None, "RMSE": R.value if fe else None}
+
     def iewpf_diagnostics_write(self, path, cycle, append=True):
         self._ck(self.L.dc_iewpf_diagnostics_write(self.h, str(path).encode(), cycle,
                                                    int(append)))

@@ -365,3 +365,39 @@ def test_twenty_cycles_bitwise(oracle):
     ge, gu, gv, gt = ens.download()
     assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
     assert np.all(gt == 20 * 300.0)
+
+
+def test_pipelined_readback_equals_synchronous_reads(oracle):
+    """dc_readback_enqueue / dc_readback_wait (two pinned slots, cycle c read while
+    cycle c+1 runs) return the same bits as the synchronous diagnostics, drifter and
+    forecast-error reads of an identical ensemble."""
+    pkg, cfg, p = setup()
+    n = 4
+    e, u, v = spread_states(oracle, p, n, 21)
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    pos = np.random.default_rng(5).uniform(0, 1, size=(n, 5, 2)) * [p.nx * p.dx, p.ny * p.dy]
+    obs = [obs_set(p, 6, 40 + c) for c in range(5)]
+    truth = [pos[0] + c * 100.0 for c in range(5)]
+    a, b = pkg.Ensemble(cfg, n), pkg.Ensemble(cfg, n)
+    for ens in (a, b):
+        ens.upload(e, u, v, 0.0)
+        ens.drifters_set(pos)
+    sync_out, pipe_out = [], []
+    for c in range(5):
+        a.da_cycle(5, obs[c], S, usig, cycle=c)
+        d, wb = a.iewpf_diagnostics()
+        gp, gw = a.drifters_get()
+        E, R, _, _ = a.forecast_error(truth[c])
+        sync_out.append((d, wb, gp, gw, E, R))
+        b.da_cycle(5, obs[c], S, usig, cycle=c)
+        b.readback_enqueue(c % 2, truth_xy=truth[c])
+        if c > 0:
+            pipe_out.append(b.readback_wait((c - 1) % 2))
+    pipe_out.append(b.readback_wait(4 % 2))
+    for (d, wb, gp, gw, E, R), r in zip(sync_out, pipe_out):
+        assert np.array_equal(d, r["diag"]) and np.array_equal(wb, r["w_beta"])
+        assert np.array_equal(gp, r["pos"]) and np.array_equal(gw, r["wind"])
+        assert E == r["E"] and R == r["RMSE"]
+    with pytest.raises(pkg.DcError):
+        b.readback_wait(0)  # nothing enqueued
