@@ -202,6 +202,13 @@ dc_status dc_residual_resample(const double* w, int32_t n, uint64_t seed, uint64
 /* Resampling by copy on the device: member m <- member idx[m] (fields, time, drifter
  * copies), local indices. Synchronous. */
 dc_status dc_resample_members(dc_ctx* ctx, const int32_t* idx);
+/* Resampling across ranks: a member's whole state -- fields, time,
+ * drifter copies -- packed into / unpacked from a device buffer of dc_member_bytes bytes
+ * (stream-ordered device copies on the context stream), so ranks can exchange resampled
+ * members over NCCL point-to-point. Import invalidates the fused CFL statistics. */
+dc_status dc_member_bytes(dc_ctx* ctx, uint64_t* bytes);
+dc_status dc_member_export(dc_ctx* ctx, int32_t m, void* d_dst);
+dc_status dc_member_import(dc_ctx* ctx, int32_t m, const void* d_src);
 /* forecast_error of the drifter copies against
  * truth positions [n_d][2]: E = sqrt(mean_d E_d), E_d = mean over members of the squared
  * minimal-image distance to truth; RMSE likewise about the ensemble mean of the unwrapped

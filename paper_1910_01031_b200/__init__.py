@@ -5,6 +5,7 @@ CUDA kernels behind the C ABI in include/driftcast_gpu.h.
 The compute lives in libdriftcast_gpu.so (C++/CUDA). This package only binds it.
 """
 from ._lib import DcError, load  # noqa: F401
+from .resample import exchange_plan, resample_across_ranks  # noqa: F401
 from .ensemble import (Config, Ensemble, forecast_error_gathered, generate_truth,  # noqa: F401
                        obs_array, pf_weights, precompute_S, precompute_local_svd, read_obs_file, residual_resample,
                        write_obs_file)

@@ -79,7 +79,8 @@ EXPORTS = [
     "dc_forecast_error", "dc_obs_file_write", "dc_obs_file_read", "dc_trajectory_write",
     "dc_set_model_error_tag", "dc_generate_truth", "dc_iewpf_set_mode",
     "dc_iewpf_diagnostics_write", "dc_drifters_get_device", "dc_forecast_error_gathered",
-    "dc_readback_enqueue", "dc_readback_wait",
+    "dc_readback_enqueue", "dc_readback_wait", "dc_member_bytes", "dc_member_export",
+    "dc_member_import",
 ]
 
 
@@ -159,6 +160,9 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "dc_resample_members": (st, [vp, ip]),
         "dc_forecast_error": (st, [vp, dp, dp, dp, dp, dp]),
         "dc_readback_enqueue": (st, [vp, C.c_int32, C.c_int32, dp]),
+        "dc_member_bytes": (st, [vp, C.POINTER(C.c_uint64)]),
+        "dc_member_export": (st, [vp, C.c_int32, vp]),
+        "dc_member_import": (st, [vp, C.c_int32, vp]),
         "dc_readback_wait": (st, [vp, C.c_int32, C.POINTER(DcParticleDiag), dp, dp, ip, dp, dp]),
         "dc_drifters_get_device": (st, [vp, vp, vp]),
         "dc_forecast_error_gathered": (st, [cfgp, C.c_int32, vp, C.c_int32, C.c_int32, vp, vp,

@@ -291,6 +291,19 @@ class Ensemble:
         self._ck(self.L.dc_forecast_error(self.h, _d(t), C.byref(E), C.byref(R), _d(ed), _d(rd)))
         return E.value, R.value, ed, rd
 
+    # ---- member state export / import (resampling across ranks) ----
+    def member_bytes(self) -> int:
+        v = C.c_uint64(0)
+        self._ck(self.L.dc_member_bytes(self.h, C.byref(v)))
+        return int(v.value)
+
+    def member_export(self, m, dev_ptr):
+        """Stream-ordered copy of member m's state into a device buffer of member_bytes()."""
+        self._ck(self.L.dc_member_export(self.h, m, C.c_void_p(dev_ptr)))
+
+    def member_import(self, m, dev_ptr):
+        self._ck(self.L.dc_member_import(self.h, m, C.c_void_p(dev_ptr)))
+
     def drifters_to_device(self, pos_ptr, wind_ptr):
         """Stream-ordered copy of the drifter ensemble into device buffers
         ([n][n_d][2] fp64 / int32), e.g. torch tensors feeding an NCCL gather."""

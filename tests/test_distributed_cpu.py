@@ -83,3 +83,65 @@ def test_two_rank_gloo_analysis_equals_single_process(oracle, tmp_path):
     assert np.array_equal(np.concatenate([q["e"] for q in parts]), e)
     assert np.array_equal(np.concatenate([q["u"] for q in parts]), u)
     assert np.array_equal(np.concatenate([q["v"] for q in parts]), v)
+
+
+# ---- resampling across ranks (paper_1910_01031_b200/resample.py) ----
+def test_exchange_plan_routes_every_slot():
+    sys.path.insert(0, os.path.dirname(HERE))
+    from paper_1910_01031_b200.resample import exchange_plan
+    per, world = 4, 3
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        idx = np.sort(rng.integers(0, per * world, per * world))
+        sent = {}
+        for r in range(world):
+            _, sends, _ = exchange_plan(idx, per, r)
+            for dest, src in sends:
+                sent.setdefault(dest, set()).add((r, src))
+        for r in range(world):
+            local, _, recvs = exchange_plan(idx, per, r)
+            got = {}
+            for sr, sl, slots in recvs:
+                assert (sr, sl) in sent.get(r, set())
+                for i in slots:
+                    got[i] = sr * per + sl
+            for i in range(per):
+                g = r * per + i
+                assert got.get(i, r * per + local[i]) == idx[g]
+            # nothing is sent to r that r does not receive
+            assert sent.get(r, set()) == {(sr, sl) for sr, sl, _ in recvs}
+
+
+def _resample_worker(rank, world, port, idx, per, outdir):
+    sys.path.insert(0, os.path.dirname(HERE))
+    import torch
+    import torch.distributed as dist
+    from paper_1910_01031_b200.resample import exchange, exchange_plan
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # stand-in members: 8-float rows carrying the global member id
+    state = torch.arange(rank * per, (rank + 1) * per, dtype=torch.float32)[:, None].repeat(1, 8)
+
+    def gather(li):
+        state.copy_(state[torch.tensor(li)])
+
+    exchange(exchange_plan(idx, per, rank), 8, lambda nb: torch.empty(nb),
+             lambda m, b: b.copy_(state[m]), gather, lambda m, b: state[m].copy_(b), dist)
+    np.save(os.path.join(outdir, f"r{rank}.npy"), state.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_resample_exchange(tmp_path):
+    """Host logic of the cross-rank resampling on CPU: every slot ends up holding the
+    member the global index names (ids carried by stand-in member buffers)."""
+    pytest.importorskip("torch")
+    import torch.multiprocessing as mp
+    world, per = 2, 5
+    idx = np.array([0, 0, 3, 6, 6, 6, 7, 9, 9, 9])  # both directions, duplicates, keeps
+    mp.spawn(_resample_worker, args=(world, _free_port(), idx, per, str(tmp_path)),
+             nprocs=world, join=True)
+    got = np.concatenate([np.load(os.path.join(tmp_path, f"r{r}.npy")) for r in range(world)])
+    assert np.array_equal(got[:, 0], idx) and np.all(got == got[:, :1])

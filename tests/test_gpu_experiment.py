@@ -307,3 +307,61 @@ def test_generate_truth_matches_oracle(oracle, tmp_path):
     assert len(recs) == len(want)
     for a, b in zip(recs, want):
         assert a[:3] == b[:3] and all(np.float64(x) == np.float64(y) for x, y in zip(a[3:], b[3:]))
+
+
+def test_resample_across_two_contexts_equals_one(oracle):
+    """Cross-rank resampling (resample.py): two contexts on one GPU stand in for two
+    ranks; members that change context travel as dc_member_export / dc_member_import
+    buffers routed by exchange_plan. Fields, times and drifter copies equal one context
+    resampling with the same global index, bit for bit."""
+    import torch
+    pkg, cfg, p = setup()
+    from paper_1910_01031_b200.resample import exchange_plan
+    n, per = 6, 3
+    e, u, v = spread_states(oracle, p, n, 9)
+    rng = np.random.default_rng(12)
+    pos = rng.uniform(0, 1, (n, 4, 2)) * [p.nx * p.dx, p.ny * p.dy]
+    whole = pkg.Ensemble(cfg, n)
+    parts = [pkg.Ensemble(cfg, per), pkg.Ensemble(cfg, per, member_base=per)]
+    whole.upload(e, u, v, 0.0)
+    whole.drifters_set(pos)
+    for r, ens in enumerate(parts):
+        ens.upload(e[r * per:(r + 1) * per], u[r * per:(r + 1) * per], v[r * per:(r + 1) * per], 0.0)
+        ens.drifters_set(pos[r * per:(r + 1) * per])
+    for ens in [whole] + parts:
+        for _ in range(2):
+            ens.advect_drifters(3000.0)
+            ens.model_step(1)
+    idx = np.array([0, 4, 4, 1, 5, 2], np.int32)  # sorted is not required by the routing
+    whole.resample_members(idx)
+    nb = parts[0].member_bytes()
+    assert nb == whole.member_bytes()
+    plans = [exchange_plan(idx, per, r) for r in range(2)]
+    wire = {}
+    for r, ens in enumerate(parts):  # exports first (the local gather overwrites members)
+        for dest, src in plans[r][1]:
+            b = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            ens.member_export(src, b.data_ptr())
+            wire[(r, src, dest)] = b
+    for r, ens in enumerate(parts):
+        ens.sync()
+    for r, ens in enumerate(parts):
+        ens.resample_members(plans[r][0])
+        for sr, sl, slots in plans[r][2]:
+            for i in slots:
+                ens.member_import(i, wire[(sr, sl, r)].data_ptr())
+        ens.sync()
+    we, wu, wv, wt = whole.download()
+    wp, ww = whole.drifters_get()
+    for r, ens in enumerate(parts):
+        ge, gu, gv, gt = ens.download()
+        gp, gw = ens.drifters_get()
+        sl = slice(r * per, (r + 1) * per)
+        assert np.array_equal(ge, we[sl]) and np.array_equal(gu, wu[sl]) and np.array_equal(gv, wv[sl])
+        assert np.array_equal(gt, wt[sl]) and np.array_equal(gp, wp[sl]) and np.array_equal(gw, ww[sl])
+    # the imported states step on like the whole ensemble (CFL statistics rescanned)
+    whole.model_step(1)
+    for ens in parts:
+        ens.model_step(1)
+    we = whole.download()[0]
+    assert np.array_equal(np.concatenate([ens.download()[0] for ens in parts]), we)
