@@ -2,6 +2,7 @@
 // C-ABI implementation (api.cu). Not part of the public boundary.
 #pragma once
 #include <atomic>
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -83,6 +84,8 @@ inline void smem_opt_in(F* func, size_t bytes) {
     const unsigned long long bit = 1ull << (dev & 63);
     if (done.load(std::memory_order_relaxed) & bit) return;
     cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (const char* c = std::getenv("DC_CARVEOUT"))  // preferred shared-memory carveout, %
+        cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(c));
     done.fetch_or(bit);
 }
 
