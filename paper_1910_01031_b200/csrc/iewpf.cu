@@ -204,10 +204,44 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
 #define DC_PULL_MIN_BLOCKS 6
 #endif
 
+__device__ __forceinline__ void cp_async8d(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+
+// Interpolation tables of every (tile, covering observation): they depend on the tile and
+// the observation's coarse alignment only, not on the particle, so they are built once per
+// analysis here instead of in every (particle, tile) CTA. One 96-thread CTA per entry
+// (warp 0 columns, warps 1-2 rows, as tile::setup).
+__global__ void __launch_bounds__(96)
+pull_tables_kernel(SweParams sp, ErrParams ep, const int4* __restrict__ lists,
+                   const int* __restrict__ counts, int n_obs, int tiles_x, tile::TabA* tabs) {
+    const int tl = blockIdx.x, li = blockIdx.y;
+    if (li >= counts[tl]) return;
+    const int4 ent = lists[static_cast<size_t>(tl) * n_obs + li];
+    const int oj = ent.y & 0xffff, ok = ent.y >> 16, ao = ent.z, bo = ent.w;
+    const int j0 = (tl % tiles_x) * TX, k0 = (tl / tiles_x) * TY;
+    const int nxc = ep.nxc, nyc = ep.nyc;
+    tile::TabA& T = tabs[static_cast<size_t>(tl) * n_obs + li];
+    // coarse indices -> the padded window (indices 11..15 read exact zeros)
+    tile::setup_cols(T, ep, sp.nx, j0, oj, [&](int a) {
+        const int da = wrapf(a - ao + WH, nxc);
+        return da < WIN ? da : WP - 1;
+    });
+    tile::setup_rows(T, ep, sp.ny, k0, ok, [&](int b) {
+        const int db = wrapf(b - bo + WH, nyc);
+        return (db < WIN ? db : WP - 1) * WP;
+    });
+}
+
 __global__ void __launch_bounds__(tile::NT, DC_PULL_MIN_BLOCKS)
 pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, int n_obs,
-                  const int4* __restrict__ lists,
-                  const int* __restrict__ counts, int tiles_x, float* eta, float* hu, float* hv,
+                  const int4* __restrict__ lists, const int* __restrict__ counts, int tiles_x,
+                  const tile::TabA* __restrict__ tabs, float* eta, float* hu, float* hv,
                   int* err, int* err_pos) {
     __shared__ double W[WP * WP];
     __shared__ tile::Smem S;
@@ -234,33 +268,42 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
             cp_async4(&ST[2][r][tx], hv + o);
         }
     }
+    // the window pad stays zero: the copies below touch only da, db < WIN
+    for (int i = tid; i < WP * WP; i += tile::NT) W[i] = 0.0;
+    __syncthreads();
+    const int4* tlist = lists + static_cast<size_t>(tl) * n_obs;
+    const tile::TabA* ttab = tabs + static_cast<size_t>(tl) * n_obs;
+    const double* wbase = win + static_cast<size_t>(m) * n_obs * (WIN * WIN);
+    auto load_win = [&](int li) {  // observation li's 11x11 window into the padded 16x16
+        if (tid < WIN * WIN)
+            cp_async8d(&W[(tid / WIN) * WP + tid % WIN],
+                       wbase + static_cast<size_t>(tlist[li].x) * (WIN * WIN) + tid);
+    };
+    auto load_tab = [&](int li) {
+        if (tid < tile::kTabChunks)
+            cp_async16(reinterpret_cast<char*>(&S.t) + 16 * tid,
+                       reinterpret_cast<const char*>(ttab + li) + 16 * tid);
+    };
+    load_win(0);
+    load_tab(0);
     asm volatile("cp.async.commit_group;\n" ::);
     bool dry = false;
     int dry_at = 0x7fffffff;
-    const int nxc = ep.nxc, nyc = ep.nyc;
     const double cy = ep.cy, cx = ep.cx, heq = ep.h_eq;
     for (int li = 0; li < cnt; ++li) {
-        const int4 ent = lists[static_cast<size_t>(tl) * n_obs + li];
-        const int o = ent.x;
-        const int oj = ent.y & 0xffff, ok = ent.y >> 16, ao = ent.z, bo = ent.w;
-        const double* wsrc = win + (static_cast<size_t>(m) * n_obs + o) * (WIN * WIN);
-        __syncthreads();  // the previous observation is done with W and the tables
-        {
-            const int da = tid % WP, db = tid / WP;  // 256 threads fill the 16x16 pad
-            W[tid] = (da < WIN && db < WIN) ? wsrc[db * WIN + da] : 0.0;
-        }
-        tile::setup(
-            S, ep, sp.nx, sp.ny, j0, k0, oj, ok,
-            [&](int a) {
-                const int da = wrapf(a - ao + WH, nxc);
-                return da < WIN ? da : WP - 1;
+        // entry li's window and tables (and, at li = 0, the tile state) have landed
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();
+        const bool more = li + 1 < cnt;
+        tile::interpolate(
+            S, [&](int brow, int a) { return W[brow + a]; },
+            [&] {  // pass 1 done: the window is free, fetch the next observation's
+                if (more) load_win(li + 1);
             },
-            [&](int b) {
-                const int db = wrapf(b - bo + WH, nyc);
-                return (db < WIN ? db : WP - 1) * WP;
+            [&] {  // pass 2 done: the tables are free
+                if (more) load_tab(li + 1);
+                asm volatile("cp.async.commit_group;\n" ::);
             });
-        tile::interpolate(S, [&](int brow, int a) { return W[brow + a]; });
-        if (li == 0) asm volatile("cp.async.wait_group 0;\n" ::);  // own cells landed
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; ++q) {
             const int r = ty + 8 * q, k = k0 + r;
@@ -622,13 +665,18 @@ void launch_tile_lists(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
     *tiles_x_out = tiles_x;
 }
 
+size_t pull_table_bytes() { return sizeof(tile::TabA); }
+
 void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep, const double* win,
                        const int* cells, int n_obs, const int* lists, const int* counts,
-                       int n_tiles, int tiles_x, float* eta, float* hu, float* hv, int* err,
-                       int* err_pos, int M) {
+                       int n_tiles, int tiles_x, void* tabs, float* eta, float* hu, float* hv,
+                       int* err, int* err_pos, int M) {
+    tile::TabA* T = static_cast<tile::TabA*>(tabs);
+    pull_tables_kernel<<<dim3(n_tiles, n_obs), 96, 0, s>>>(
+        sp, ep, reinterpret_cast<const int4*>(lists), counts, n_obs, tiles_x, T);
     pull_apply_kernel<<<dim3(n_tiles, M), 256, 0, s>>>(sp, ep, win, n_obs,
                                                        reinterpret_cast<const int4*>(lists), counts,
-                                                       tiles_x, eta, hu, hv, err, err_pos);
+                                                       tiles_x, T, eta, hu, hv, err, err_pos);
 }
 
 void launch_perp_pair(cudaStream_t s, const ErrParams& ep, uint64_t seed, int64_t member_base,

@@ -16,6 +16,7 @@ struct IewpfBuffers {
     double* win = nullptr;    // [M][n_obs][121] pull windows (SOAR(SOAR(dipole)))
     int* tile_lists = nullptr;// [n_tiles][cap_obs] int4 {obs id, oj | ok << 16, ao, bo}, ascending id
     int* tile_count = nullptr;// [n_tiles]
+    void* tabs = nullptr;     // [n_tiles][cap_obs] interpolation tables of the pull
     double* nu = nullptr;     // [M][nr]
     double* scal = nullptr;   // [M][8]: c, phi, gamma, zeta, alpha, xx, nn, nx
     double* cz = nullptr;     // [M][2] local (c, zeta)
@@ -89,7 +90,7 @@ inline void fe_free(FeScratch& f) {
 }
 
 inline void iewpf_free(IewpfBuffers& b) {
-    void* ps[] = {b.obs, b.cells, b.d, b.sd, b.win, b.tile_lists, b.tile_count, b.nu, b.scal,
+    void* ps[] = {b.obs, b.cells, b.d, b.sd, b.win, b.tile_lists, b.tile_count, b.tabs, b.nu, b.scal,
                   b.cz, b.cz_all, b.wb, b.S, b.usig, b.foffs, b.dpos, b.dwind, b.z, b.bad,
                   b.lb_order, b.lb_start};
     for (void* p : ps)

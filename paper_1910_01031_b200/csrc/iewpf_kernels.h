@@ -17,10 +17,13 @@ void launch_pull_windows(cudaStream_t s, const ErrParams& ep, const double* sd, 
                          double* win, const int* err, int M);
 void launch_tile_lists(cudaStream_t s, const SweParams& sp, const ErrParams& ep, const int* cells,
                        int n_obs, int* lists, int* counts, int* n_tiles_out, int* tiles_x_out);
+// pull_tables (member-independent interpolation tables of every (tile, covering obs),
+// tabs: n_tiles x n_obs x pull_table_bytes()) + pull_apply
+size_t pull_table_bytes();
 void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep, const double* win,
                        const int* cells, int n_obs, const int* lists, const int* counts,
-                       int n_tiles, int tiles_x, float* eta, float* hu, float* hv, int* err,
-                       int* err_pos, int M);
+                       int n_tiles, int tiles_x, void* tabs, float* eta, float* hu, float* hv,
+                       int* err, int* err_pos, int M);
 void launch_perp_pair(cudaStream_t s, const ErrParams& ep, uint64_t seed, int64_t member_base,
                       uint64_t cycle, double ratio, double* xi, double* nu, int* foffs,
                       double* scal, const int* err, int M);

@@ -27,9 +27,9 @@ constexpr int XW = TX + 2;         // tile width incl. halo
 constexpr int YH = TY + 2;         // tile height incl. halo (= 32: one lane per row)
 constexpr int NT = 256;            // threads
 
-struct Smem {
-    double X[NBMAX][XW];
-    double D[YH][XW];
+// the interpolation tables of one (tile, coarse alignment): member-independent for the
+// IEWPF pull, so pull_apply reads them precomputed (pull_tables_kernel)
+struct Tab {
     double ct[XW];           // x fraction per halo column
     double rt[YH];           // y fraction per halo row
     int cg_a[XW][4];         // per column group: coarse columns a0-1 .. a0+2 (mapped)
@@ -38,6 +38,14 @@ struct Smem {
     int rg_first[YH + 1];    // first halo row of each row group (+ end sentinel)
     int brow[NBMAX];         // coarse row of each X slot (mapped)
     int nb, ncg, nrg;
+};
+struct alignas(16) TabA : Tab {};  // 16-byte aligned, copied with 16-byte cp.async
+constexpr int kTabChunks = (sizeof(TabA) + 15) / 16;
+
+struct Smem {
+    double X[NBMAX][XW];
+    double D[YH][XW];
+    TabA t;
 };
 
 struct Cm {
@@ -73,7 +81,7 @@ __device__ __forceinline__ unsigned lanemask_le() {
 // Column tables of one tile (warp 0): depend only on the tile's columns and the coarse
 // column offset, so a CTA that streams down a column strip builds them once. No barrier.
 template <class COLMAP>
-__device__ __forceinline__ void setup_cols(Smem& S, const ErrParams& ep, int nx, int j0, int oj,
+__device__ __forceinline__ void setup_cols(Tab& S, const ErrParams& ep, int nx, int j0, int oj,
                                            COLMAP colmap) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) {  // columns l and 32+l (l < 2) (stochastic.hpp:104-108)
@@ -121,7 +129,7 @@ __device__ __forceinline__ void setup_cols(Smem& S, const ErrParams& ep, int nx,
 
 // Row tables of one tile (warps 1, 2). No barrier.
 template <class ROWMAP>
-__device__ __forceinline__ void setup_rows(Smem& S, const ErrParams& ep, int ny, int k0, int ok,
+__device__ __forceinline__ void setup_rows(Tab& S, const ErrParams& ep, int ny, int k0, int ok,
                                            ROWMAP rowmap) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool whole = ep.nyc <= NBMAX;
@@ -168,35 +176,45 @@ __device__ __forceinline__ void setup_rows(Smem& S, const ErrParams& ep, int ny,
 template <class COLMAP, class ROWMAP>
 __device__ __forceinline__ void setup(Smem& S, const ErrParams& ep, int nx, int ny, int j0,
                                       int k0, int oj, int ok, COLMAP colmap, ROWMAP rowmap) {
-    setup_cols(S, ep, nx, j0, oj, colmap);
-    setup_rows(S, ep, ny, k0, ok, rowmap);
+    setup_cols(S.t, ep, nx, j0, oj, colmap);
+    setup_rows(S.t, ep, ny, k0, ok, rowmap);
     __syncthreads();
 }
 
-// Passes 1 and 2 into S.D. VALF(mapped row, mapped col) returns the coarse value.
-// Ends with a barrier.
-template <class VALF>
-__device__ __forceinline__ void interpolate(Smem& S, VALF valf) {
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+// Passes 1 and 2 into S.D from the tables in S.t. VALF(mapped row, mapped col) returns the
+// coarse value. Ends with a barrier. after1 runs right after the barrier that ends pass 1
+// (the coarse values are no longer read), after2 after the final barrier (the tables are
+// no longer read) -- where pull_apply prefetches the next observation's window / tables.
+template <class VALF, class H1 = NoHook, class H2 = NoHook>
+__device__ __forceinline__ void interpolate(Smem& S, VALF valf, H1 after1 = H1{},
+                                            H2 after2 = H2{}) {
+    const Tab& T = S.t;
     const int tid = threadIdx.x;
-    const int ncg = S.ncg, n1 = S.nb * ncg;
+    const int ncg = T.ncg, n1 = T.nb * ncg;
     for (int i = tid; i < n1; i += NT) {  // (X slot, column group)
         const int s = i / ncg, g = i - s * ncg;
-        const int b = S.brow[s];
-        const Cm m = coef(valf(b, S.cg_a[g][0]), valf(b, S.cg_a[g][1]), valf(b, S.cg_a[g][2]),
-                          valf(b, S.cg_a[g][3]));
-        const int j1 = S.cg_first[g + 1];
-        for (int jl = S.cg_first[g]; jl < j1; ++jl) S.X[s][jl] = eval(m, S.ct[jl]);
+        const int b = T.brow[s];
+        const Cm m = coef(valf(b, T.cg_a[g][0]), valf(b, T.cg_a[g][1]), valf(b, T.cg_a[g][2]),
+                          valf(b, T.cg_a[g][3]));
+        const int j1 = T.cg_first[g + 1];
+        for (int jl = T.cg_first[g]; jl < j1; ++jl) S.X[s][jl] = eval(m, T.ct[jl]);
     }
     __syncthreads();
-    const int n2 = S.nrg * XW;
+    after1();
+    const int n2 = T.nrg * XW;
     for (int i = tid; i < n2; i += NT) {  // (row group, halo column)
         const int g = i / XW, jl = i - g * XW;
-        const Cm m = coef(S.X[S.rg_sl[g][0]][jl], S.X[S.rg_sl[g][1]][jl], S.X[S.rg_sl[g][2]][jl],
-                          S.X[S.rg_sl[g][3]][jl]);
-        const int r1 = S.rg_first[g + 1];
-        for (int r = S.rg_first[g]; r < r1; ++r) S.D[r][jl] = eval(m, S.rt[r]);
+        const Cm m = coef(S.X[T.rg_sl[g][0]][jl], S.X[T.rg_sl[g][1]][jl], S.X[T.rg_sl[g][2]][jl],
+                          S.X[T.rg_sl[g][3]][jl]);
+        const int r1 = T.rg_first[g + 1];
+        for (int r = T.rg_first[g]; r < r1; ++r) S.D[r][jl] = eval(m, T.rt[r]);
     }
     __syncthreads();
+    after2();
 }
 
 } // namespace tile
