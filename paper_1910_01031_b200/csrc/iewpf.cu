@@ -193,7 +193,8 @@ __global__ void tile_lists_kernel(SweParams sp, ErrParams ep, const int* __restr
 // Sequential-equivalent gather of every covering observation's pull into one tile of one
 // particle (optimal_proposal_pull, SPEC.md:455-463 + add_q_half, stochastic.hpp:144-160).
 constexpr int WP = 16;  // padded window pitch: indices 11..15 read exact zeros
-constexpr int kRowsPerThread = (TY + 7) / 8;
+using tile::kRowsPerThread;
+using tile::kWarps;
 
 __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -260,7 +261,7 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
     // for occupancy, and no barrier is needed since only the owner touches them
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = ty + 8 * q, k = k0 + r;
+        const int r = ty + kWarps * q, k = k0 + r;
         if (r < TY && k < sp.ny && j < sp.nx) {
             const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
             cp_async4(&ST[0][r][tx], eta + o);
@@ -306,7 +307,7 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
             });
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; ++q) {
-            const int r = ty + 8 * q, k = k0 + r;
+            const int r = ty + kWarps * q, k = k0 + r;
             if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
             const int rr = r + 1, jl = tx + 1;
             const double de = S.D[rr][jl];
@@ -324,7 +325,7 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
     }
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = ty + 8 * q, k = k0 + r;
+        const int r = ty + kWarps * q, k = k0 + r;
         if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
         const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
         eta[o] = ST[0][r][tx];
@@ -674,7 +675,7 @@ void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
     tile::TabA* T = static_cast<tile::TabA*>(tabs);
     pull_tables_kernel<<<dim3(n_tiles, n_obs), 96, 0, s>>>(
         sp, ep, reinterpret_cast<const int4*>(lists), counts, n_obs, tiles_x, T);
-    pull_apply_kernel<<<dim3(n_tiles, M), 256, 0, s>>>(sp, ep, win, n_obs,
+    pull_apply_kernel<<<dim3(n_tiles, M), tile::NT, 0, s>>>(sp, ep, win, n_obs,
                                                        reinterpret_cast<const int4*>(lists), counts,
                                                        tiles_x, T, eta, hu, hv, err, err_pos);
 }

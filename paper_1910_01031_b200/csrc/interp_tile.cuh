@@ -25,7 +25,12 @@ constexpr int TX = 32, TY = 30;    // output tile (TY+2 = 32 halo rows)
 constexpr int NBMAX = TY + 2 + 3;  // coarse rows a tile can touch (c_omega = 1 worst case)
 constexpr int XW = TX + 2;         // tile width incl. halo
 constexpr int YH = TY + 2;         // tile height incl. halo (= 32: one lane per row)
-constexpr int NT = 256;            // threads
+#ifndef DC_TILE_NT
+#define DC_TILE_NT 256
+#endif
+constexpr int NT = DC_TILE_NT;     // threads (a multiple of 32, >= 96)
+constexpr int kWarps = NT / 32;    // warps; the apply phase gives warp w rows w, w + kWarps, ..
+constexpr int kRowsPerThread = (TY + kWarps - 1) / kWarps;
 
 // the interpolation tables of one (tile, coarse alignment): member-independent for the
 // IEWPF pull, so pull_apply reads them precomputed (pull_tables_kernel)

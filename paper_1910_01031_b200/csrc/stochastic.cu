@@ -145,7 +145,8 @@ __device__ __forceinline__ unsigned ordered_bits(float f) {
 // Q^{1/2} tail + add (stochastic.hpp:144-160) for one (member, 32x30 tile). When mx is
 // given, also reduces the CFL statistics of the NEW state (Stepper::load,
 // swe.hpp:306-317) so the next model step needs no separate scan.
-constexpr int kRowsPerThread = (TY + 7) / 8;  // 4
+using tile::kRowsPerThread;
+using tile::kWarps;
 #ifndef DC_QHALF_MIN_BLOCKS
 #define DC_QHALF_MIN_BLOCKS 6
 #endif
@@ -156,7 +157,7 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
                     float* hv, int* err, int* err_pos, unsigned* mx) {
     __shared__ tile::Smem S;
     __shared__ float ST[3][TY][TX];
-    __shared__ float red[3][8];
+    __shared__ float red[3][kWarps];
     const int m = blockIdx.z;
     // another tile of the member may raise E_DRY_ADD meanwhile: decide once per CTA
     if (__syncthreads_or(err[m] != 0)) return;
@@ -166,11 +167,11 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
     const size_t pitch = sp.pitch;
     // this thread's cells: column j, rows k0 + ty + 8q
     const size_t cell0 = static_cast<size_t>(m) * sp.ny * pitch + static_cast<size_t>(k0 + ty) * pitch + j;
-    const size_t step = 8 * pitch;
+    const size_t step = static_cast<size_t>(kWarps) * pitch;
     bool okq[kRowsPerThread];
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = ty + 8 * q;
+        const int r = ty + kWarps * q;
         okq[q] = (r < TY) && (k0 + r < sp.ny) && (j < sp.nx);
     }
     // stage the tile's state in shared memory with cp.async first: the loads' latency
@@ -179,7 +180,7 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
     for (int q = 0; q < kRowsPerThread; ++q) {
         if (!okq[q]) continue;
         const size_t o = cell0 + q * step;
-        const int r = ty + 8 * q;
+        const int r = ty + kWarps * q;
         cp_async4(&ST[0][r][tx], eta + o);
         cp_async4(&ST[1][r][tx], hu + o);
         cp_async4(&ST[2][r][tx], hv + o);
@@ -200,7 +201,7 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
         if (!okq[q]) continue;
-        const int rr = ty + 8 * q + 1, jl = tx + 1;
+        const int rr = ty + kWarps * q + 1, jl = tx + 1;
         const double de = S.D[rr][jl];
         const double dhu = -cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
         const double dhv = cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
@@ -244,7 +245,7 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
         __syncthreads();
         if (threadIdx.x == 0) {
             float a = red[0][0], b = red[1][0], c = red[2][0];
-            for (int i = 1; i < 8; ++i) {
+            for (int i = 1; i < kWarps; ++i) {
                 a = fmaxf(a, red[0][i]);
                 b = fmaxf(b, red[1][i]);
                 c = fminf(c, red[2][i]);
@@ -286,7 +287,7 @@ void launch_q_half_apply(cudaStream_t s, const SweParams& sp, const ErrParams& e
                          const double* corr, const int* offsets, double scale, float* eta,
                          float* hu, float* hv, int* err, int* err_pos, int M, unsigned* mx) {
     dim3 grid((sp.nx + TX - 1) / TX, (sp.ny + TY - 1) / TY, M);
-    q_half_apply_kernel<<<grid, 256, 0, s>>>(sp, ep, corr, offsets, scale, eta, hu, hv, err,
+    q_half_apply_kernel<<<grid, tile::NT, 0, s>>>(sp, ep, corr, offsets, scale, eta, hu, hv, err,
                                              err_pos, mx);
 }
 
