@@ -932,7 +932,7 @@ int64_t dc_kernel_launches(dc_ctx* ctx) {
     // graph path: 2 kernels per step + 2 per substep iteration (3 with the separate
     // substep_end), iterations counted on the device
     unsigned long long iters = 0;
-    if (ctx->use_graph && ctx->substep_iters) {
+    if (ctx->use_graph && !ctx->persist && ctx->substep_iters) {  // persistent: 1 per step
         cudaMemcpyAsync(&iters, ctx->substep_iters, sizeof(iters), cudaMemcpyDeviceToHost,
                         ctx->stream);
         cudaStreamSynchronize(ctx->stream);
