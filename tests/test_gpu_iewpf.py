@@ -401,3 +401,40 @@ def test_pipelined_readback_equals_synchronous_reads(oracle):
         assert E == r["E"] and R == r["RMSE"]
     with pytest.raises(pkg.DcError):
         b.readback_wait(0)  # nothing enqueued
+
+
+@pytest.mark.timeout(600)
+def test_da_cycle_refined_grid_moorings_bitwise(oracle):
+    """configs[4] geometry: the 4x refined grid (1000x600, dx = dy = 1110 m, 13 substeps
+    per model step, N_R = 24,000) with 240 moorings on a 20x12 lattice: one DA cycle for 2
+    members, state and diagnostics bitwise equal to the oracle."""
+    pkg = _gpu()
+    cfg = pkg.Config(nx=1000, ny=600, dx=1110.0, dy=1110.0)
+    p = make_params(nx=1000, ny=600, dx=1110.0, dy=1110.0, q0=cfg.q0, seed=cfg.seed,
+                    c_omega=cfg.c_omega)
+    n = 2
+    e, u, v = spread_states(oracle, p, n, 41)
+    lx, ly = p.nx * p.dx, p.ny * p.dy
+    X, Y = np.meshgrid((np.arange(20) + 0.5) / 20 * lx, (np.arange(12) + 0.5) / 12 * ly)
+    lat = np.stack([X.ravel(), Y.ravel()], 1)
+    obs = np.hstack([lat, np.random.default_rng(43).normal(0, 20.0, (240, 2))])
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    ens.da_cycle(5, obs, S, usig, cycle=2)
+    ge, gu, gv, gt = ens.download()
+    diag, wb = ens.iewpf_diagnostics()
+    subs = ens.substeps()
+    oe, ou, ov = e.copy(), u.copy(), v.copy()
+    for m in range(n):
+        s = State(oe[m], ou[m], ov[m], 0.0)
+        for i in range(5):
+            oracle.model_step(p, s, 1)
+            if i < 4:
+                oracle.perturb_philox(p, s, m, i)
+    od, owb = oracle.iewpf_assimilate(p, oe, ou, ov, obs, S, usig, 2)
+    assert np.all(subs >= 12)  # the refined grid's CFL: 13 substeps per 60 s
+    assert np.array_equal(wb, owb) and np.array_equal(diag, od)
+    assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
+    assert np.all(gt == 300.0)
