@@ -438,3 +438,39 @@ def test_da_cycle_refined_grid_moorings_bitwise(oracle):
     assert np.array_equal(wb, owb) and np.array_equal(diag, od)
     assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
     assert np.all(gt == 300.0)
+
+
+@pytest.mark.timeout(600)
+def test_iewpf_observation_count_edges(oracle):
+    """The observation-count range of one analysis: 1 and the maximum 1024 (every tile
+    covered by every observation, 1024-deep pull folds) bitwise vs the oracle; 0, 1025
+    and a non-finite position rejected with DC_EINVAL before any device work."""
+    pkg, cfg, p = setup()
+    n = 2
+    e, u, v = spread_states(oracle, p, n, 51)
+    _, S = oracle.precompute_S(p)
+    usig = np.linalg.cholesky(oracle.local_block(p, S))
+    for n_obs in (1, 1024):
+        obs = obs_set(p, n_obs, 60 + n_obs)
+        ens = pkg.Ensemble(cfg, n)
+        ens.upload(e, u, v, 0.0)
+        ens.iewpf_assimilate(obs, S, usig, cycle=1)
+        ge, gu, gv, _ = ens.download()
+        diag, wb = ens.iewpf_diagnostics()
+        oe, ou, ov = e.copy(), u.copy(), v.copy()
+        od, owb = oracle.iewpf_assimilate(p, oe, ou, ov, obs, S, usig, 1)
+        assert np.array_equal(wb, owb) and np.array_equal(diag, od), n_obs
+        assert np.array_equal(ge, oe) and np.array_equal(gu, ou) and np.array_equal(gv, ov)
+        ens.close()
+    ens = pkg.Ensemble(cfg, n)
+    ens.upload(e, u, v, 0.0)
+    bad = [obs_set(p, 1025, 3), np.zeros((0, 4))]
+    nan = obs_set(p, 4, 4)
+    nan[2, 0] = np.nan
+    bad.append(nan)
+    for obs in bad:
+        with pytest.raises(pkg.DcError) as ei:
+            ens.iewpf_assimilate(obs, S, usig, cycle=1)
+        assert ei.value.status == 1, ei.value  # DC_EINVAL
+    ge, _, _, _ = ens.download()
+    assert np.array_equal(ge, e)  # nothing was applied
