@@ -30,8 +30,10 @@ struct dc_ctx {
     SweParams sp{};
     ErrParams ep{};
     int nr = 0;
-    size_t field_elems = 0;
-    float* f[6] = {nullptr};  // eta, hu, hv, stage eta, stage hu, stage hv
+    size_t field_elems = 0;   // floats per field (M x mstride)
+    float* blk[2] = {nullptr};  // the two state sets (psi^n, psi*), 3 fields each
+    float* f[6] = {nullptr};  // eta, hu, hv, stage eta, stage hu, stage hv (views into blk)
+    CUtensorMap maps[2];      // TMA maps of the two state sets (stage kernels)
     StepCtl ctl{};
     void* ctl_mem = nullptr;
     unsigned long long* substep_iters = nullptr; // device counters (graph path): [iters, member-substeps]
@@ -53,13 +55,8 @@ struct dc_ctx {
     bool use_graph = true;
     int64_t launches = 0;
     int last_max_sub = 8;
-    // substep end fused into stage 2 (DC_FUSED_END=0: the separate substep_end launch)
-    bool fused_end = true;
     // CTA row units of the SWE stage grid (big strips first, short ones last)
     int2* units = nullptr;
-    // persistent model step (DC_PERSISTENT): grid and row strips per member
-    bool persist = false;
-    int p_grid = 0, p_nsp = 1;
     // IEWPF / observation / drifter state
     IewpfBuffers iw{};
     FeScratch fe{};  // forecast_error scratch
@@ -145,7 +142,8 @@ void derive_params(dc_ctx* c) {
     SweParams& P = c->sp;
     P.nx = g.nx;
     P.ny = g.ny;
-    P.pitch = (g.nx + 31) / 32 * 32;
+    P.pitch = (g.nx + 4 + 31) / 32 * 32;  // + the 2-cell ghost frame on both sides
+    P.mstride = static_cast<size_t>(g.ny + 4) * P.pitch;
     P.M = c->M;
     P.strips = (g.ny + 31) / 32;
     P.by = (g.ny + P.strips - 1) / P.strips;
@@ -240,6 +238,23 @@ dc_status check_member(dc_ctx* ctx, int m) {
     return DC_OK;
 }
 
+// The two stages of one substep: psi^n (set 0) -> psi* (set 1) -> psi^n+1 (set 0).
+void launch_stage1(dc_ctx* ctx, cudaStream_t s) {
+    const CUtensorMap maps[2] = {ctx->maps[0], ctx->maps[0]};
+    launch_stage(s, ctx->sp, ctx->exact, 1, maps, ctx->f[0], ctx->f[1], ctx->f[2], ctx->f[3],
+                 ctx->f[4], ctx->f[5], ctx->ctl);
+}
+void launch_stage2(dc_ctx* ctx, cudaStream_t s, unsigned long long cond, int end_mode) {
+    const CUtensorMap maps[2] = {ctx->maps[1], ctx->maps[0]};
+    launch_stage(s, ctx->sp, ctx->exact, 2, maps, ctx->f[3], ctx->f[4], ctx->f[5], ctx->f[0],
+                 ctx->f[1], ctx->f[2], ctx->ctl, cond, end_mode);
+}
+
+// the ghost frame of the model state (every writer but the stage kernels leaves it stale)
+void fix_ghosts(dc_ctx* ctx, cudaStream_t s) {
+    launch_fix_ghosts(s, ctx->sp, ctx->f[0], ctx->field_elems);
+}
+
 // One model step as a graph: [reset + cfl_scan] -> step_begin -> while(any active){stage1,
 // stage2, substep_end}. The while condition is set on the device by substep_end. The
 // scan is skipped when the kernel that last changed the state already reduced the CFL
@@ -247,6 +262,7 @@ dc_status check_member(dc_ctx* ctx, int m) {
 dc_status build_step_graph(dc_ctx* ctx, bool with_scan, cudaGraphExec_t* exec) {
     cudaStream_t s = ctx->stream;
     CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    fix_ghosts(ctx, s);
     if (with_scan) {
         launch_reset_stats(s, ctx->sp, ctx->ctl);
         launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
@@ -259,7 +275,7 @@ dc_status build_step_graph(dc_ctx* ctx, bool with_scan, cudaGraphExec_t* exec) {
     cudaGraphConditionalHandle handle;
     CU(cudaGraphConditionalHandleCreate(&handle, cap, 1, cudaGraphCondAssignDefault));
     const unsigned long long h = static_cast<unsigned long long>(handle);
-    launch_step_begin(s, ctx->sp, ctx->ctl, h, ctx->fused_end ? 1 : 0);
+    launch_step_begin(s, ctx->sp, ctx->ctl, h, 1);
     CU(cudaStreamGetCaptureInfo(s, &st, nullptr, &cap, &deps, &ndeps));
     cudaGraphNodeParams cp{};
     cp.type = cudaGraphNodeTypeConditional;
@@ -273,12 +289,8 @@ dc_status build_step_graph(dc_ctx* ctx, bool with_scan, cudaGraphExec_t* exec) {
     cudaStream_t bs;
     CU(cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking));
     CU(cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    launch_stage(bs, ctx->sp, ctx->exact, 1, ctx->f[0], ctx->f[1], ctx->f[2], nullptr, nullptr,
-                 nullptr, ctx->f[3], ctx->f[4], ctx->f[5], ctx->ctl);
-    launch_stage(bs, ctx->sp, ctx->exact, 2, ctx->f[3], ctx->f[4], ctx->f[5], ctx->f[0],
-                 ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl, h,
-                 ctx->fused_end ? 2 : 0);
-    if (!ctx->fused_end) launch_substep_end(bs, ctx->sp, ctx->ctl, h, 1);
+    launch_stage1(ctx, bs);
+    launch_stage2(ctx, bs, h, 2);
     cudaGraph_t body_out = nullptr;
     CU(cudaStreamEndCapture(bs, &body_out));
     CU(cudaStreamDestroy(bs));
@@ -293,6 +305,8 @@ dc_status build_step_graph(dc_ctx* ctx, bool with_scan, cudaGraphExec_t* exec) {
 // then confirm on the host and continue one substep at a time.
 dc_status step_host_loop(dc_ctx* ctx, bool with_scan) {
     cudaStream_t s = ctx->stream;
+    fix_ghosts(ctx, s);
+    ctx->launches += 1;
     if (with_scan) {
         launch_reset_stats(s, ctx->sp, ctx->ctl);
         launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
@@ -304,16 +318,9 @@ dc_status step_host_loop(dc_ctx* ctx, bool with_scan) {
     int guess = ctx->last_max_sub;
     while (true) {
         for (int i = 0; i < guess; ++i) {
-            launch_stage(s, ctx->sp, ctx->exact, 1, ctx->f[0], ctx->f[1], ctx->f[2], nullptr,
-                         nullptr, nullptr, ctx->f[3], ctx->f[4], ctx->f[5], ctx->ctl);
-            launch_stage(s, ctx->sp, ctx->exact, 2, ctx->f[3], ctx->f[4], ctx->f[5], ctx->f[0],
-                         ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl, 0ull,
-                         ctx->fused_end ? 1 : 0);
+            launch_stage1(ctx, s);
+            launch_stage2(ctx, s, 0ull, 1);
             ctx->launches += 2;
-            if (!ctx->fused_end) {
-                launch_substep_end(s, ctx->sp, ctx->ctl, 0ull, 0);
-                ctx->launches += 1;
-            }
         }
         done += guess;
         int any = 0;
@@ -400,10 +407,10 @@ dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base
     ctx->base = member_base;
     ctx->device = device;
     ctx->exact = cfg->exact_fp != 0;
+    // DC_NO_GRAPH=1: the host-driven substep loop (profiling: ncu does not descend into
+    // the conditional node of the step graph)
     const char* ng = std::getenv("DC_NO_GRAPH");
     ctx->use_graph = !(ng && ng[0] == '1');
-    const char* fe = std::getenv("DC_FUSED_END");
-    ctx->fused_end = !(fe && fe[0] == '0');
     derive_params(ctx);
     *out = ctx;
     int prev_dev = -1;
@@ -437,13 +444,6 @@ static void choose_strips(SweParams& P, int sms, int per_sm) {
             P.strips = strips;
         }
     }
-    if (const char* sr = std::getenv("DC_STRIP_ROWS")) {  // fixed strip height (experiments)
-        const int by = std::atoi(sr);
-        if (by >= 4 && by <= P.ny) {
-            P.by = by;
-            P.strips = (P.ny + by - 1) / by;
-        }
-    }
 }
 
 // Row units {m, y0 | y1 << 16} of the stage grid: every member's rows as big strips (the
@@ -475,14 +475,6 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         choose_strips(ctx->sp, sms, swe_stage_occupancy());
-        const char* pe = std::getenv("DC_PERSISTENT");
-        ctx->persist = pe && std::atoi(pe) != 0;
-        if (ctx->persist) {
-            ctx->p_grid = sms * swe_persistent_occupancy();
-            const char* pr = std::getenv("DC_PSTRIP_ROWS");
-            const int rows = std::max(4, pr ? std::atoi(pr) : 75);
-            ctx->p_nsp = std::max(1, std::min(ctx->sp.ny / 4, (ctx->sp.ny + rows / 2) / rows));
-        }
     }
     // CTA rows of the stage grid (members x strips, plus two tail strips per member) must
     // fit gridDim.y
@@ -491,12 +483,10 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
                        "too many members for one context (members x strips > 65535): split "
                        "them over several contexts / GPUs");
     {
-        const char* tr = std::getenv("DC_TAIL_ROWS");
-        const char* ts = std::getenv("DC_TAIL_STRIPS");
-        // default: two short strips of ~2/5 of a big strip per member (measured 2.6 % per
-        // model step at 500x300 x 100 members; DC_TAIL_ROWS=0 restores uniform strips)
-        const int tail_rows = tr ? std::atoi(tr) : std::max(4, (2 * ctx->sp.by) / 5);
-        const int n_tail = ts ? std::atoi(ts) : (ctx->sp.ny >= 4 * ctx->sp.by ? 2 : 0);
+        // two short strips of ~2/5 of a big strip per member (measured 2.6 % per model
+        // step at 500x300 x 100 members against uniform strips)
+        const int tail_rows = std::max(4, (2 * ctx->sp.by) / 5);
+        const int n_tail = ctx->sp.ny >= 4 * ctx->sp.by ? 2 : 0;
         if (tail_rows > 0 && n_tail > 0 && tail_rows * n_tail < ctx->sp.ny && ctx->sp.ny < 32768) {
             const std::vector<int2> u = build_units(ctx->sp, tail_rows, n_tail);
             CU(cudaMalloc(&ctx->units, u.size() * sizeof(int2)));
@@ -511,10 +501,18 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
         CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         ctx->own_stream = true;
     }
-    ctx->field_elems = static_cast<size_t>(ctx->M) * ctx->sp.ny * ctx->sp.pitch;
-    for (int i = 0; i < 6; ++i) {
-        CU(cudaMalloc(&ctx->f[i], ctx->field_elems * sizeof(float)));
-        CU(cudaMemsetAsync(ctx->f[i], 0, ctx->field_elems * sizeof(float), ctx->stream));
+    ctx->field_elems = static_cast<size_t>(ctx->M) * ctx->sp.mstride;
+    // each state set is one allocation of 3 fields field_elems apart, so one 3-D TMA box
+    // brings rows of all three fields; field pointers address cell (0, 0) inside the
+    // 2-cell ghost frame (SweParams::mstride)
+    const size_t origin = 2 * static_cast<size_t>(ctx->sp.pitch) + 2;
+    for (int s = 0; s < 2; ++s) {
+        const size_t bytes = 3 * ctx->field_elems * sizeof(float);
+        CU(cudaMalloc(&ctx->blk[s], bytes));
+        CU(cudaMemsetAsync(ctx->blk[s], 0, bytes, ctx->stream));
+        for (int i = 0; i < 3; ++i) ctx->f[3 * s + i] = ctx->blk[s] + i * ctx->field_elems + origin;
+        if (!make_state_map(&ctx->maps[s], ctx->blk[s], ctx->sp, ctx->field_elems))
+            return set_err(ctx, DC_ECUDA, "cuTensorMapEncodeTiled failed for the state maps");
     }
     const int M = ctx->M;
     // 17 arrays, each rounded up to 16 bytes by take()
@@ -540,10 +538,6 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     ctx->ctl.any_active = reinterpret_cast<int*>(take(sizeof(int)));
     ctx->ctl.n_active = reinterpret_cast<int*>(take(sizeof(int)));
     ctx->ctl.mdone = reinterpret_cast<unsigned*>(take(M * sizeof(unsigned)));
-    ctx->ctl.next = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long)));
-    ctx->ctl.s1c = reinterpret_cast<unsigned*>(take(M * sizeof(unsigned)));
-    ctx->ctl.dsub = reinterpret_cast<int*>(take(M * sizeof(int)));
-    ctx->ctl.hang = reinterpret_cast<int*>(take(sizeof(int)));
     CU(cudaMalloc(&ctx->substep_iters, 2 * sizeof(unsigned long long)));
     CU(cudaMalloc(&ctx->host_iters, 2 * sizeof(unsigned long long)));
     CU(cudaMemsetAsync(ctx->host_iters, 0, 2 * sizeof(unsigned long long), ctx->stream));
@@ -576,7 +570,7 @@ dc_status dc_destroy(dc_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->step_exec) cudaGraphExecDestroy(ctx->step_exec);
     if (ctx->step_exec_fused) cudaGraphExecDestroy(ctx->step_exec_fused);
-    for (auto* q : ctx->f) cudaFree(q);
+    for (auto* q : ctx->blk) cudaFree(q);
     cudaFree(ctx->ctl_mem);
     if (ctx->units) cudaFree(ctx->units);
     cudaFree(ctx->substep_iters);
@@ -612,7 +606,7 @@ dc_status dc_upload_member(dc_ctx* ctx, int32_t m, const float* eta, const float
     DeviceGuard dg_(ctx);
     dc_status st = check_member(ctx, m);
     if (st) return st;
-    const size_t off = static_cast<size_t>(m) * ctx->sp.ny * ctx->sp.pitch;
+    const size_t off = static_cast<size_t>(m) * ctx->sp.mstride;
     const float* src[3] = {eta, hu, hv};
     for (int i = 0; i < 3; ++i)
         CU(cudaMemcpy2DAsync(ctx->f[i] + off, ctx->sp.pitch * sizeof(float), src[i],
@@ -628,11 +622,13 @@ dc_status dc_upload_all(dc_ctx* ctx, const float* eta, const float* hu, const fl
                         const double* t) {
     DeviceGuard dg_(ctx);
     const float* src[3] = {eta, hu, hv};
-    for (int i = 0; i < 3; ++i)
-        CU(cudaMemcpy2DAsync(ctx->f[i], ctx->sp.pitch * sizeof(float), src[i],
-                             ctx->sp.nx * sizeof(float), ctx->sp.nx * sizeof(float),
-                             static_cast<size_t>(ctx->sp.ny) * ctx->M, cudaMemcpyHostToDevice,
-                             ctx->stream));
+    const size_t cells = static_cast<size_t>(ctx->sp.nx) * ctx->sp.ny;
+    for (int m = 0; m < ctx->M; ++m)
+        for (int i = 0; i < 3; ++i)
+            CU(cudaMemcpy2DAsync(ctx->f[i] + m * ctx->sp.mstride, ctx->sp.pitch * sizeof(float),
+                                 src[i] + m * cells, ctx->sp.nx * sizeof(float),
+                                 ctx->sp.nx * sizeof(float), ctx->sp.ny, cudaMemcpyHostToDevice,
+                                 ctx->stream));
     if (t)
         CU(cudaMemcpyAsync(ctx->ctl.t, t, ctx->M * sizeof(double), cudaMemcpyHostToDevice,
                            ctx->stream));
@@ -646,7 +642,7 @@ dc_status dc_download_member(dc_ctx* ctx, int32_t m, float* eta, float* hu, floa
     dc_status st = check_member(ctx, m);
     if (st) return st;
     st = surface_errors(ctx);
-    const size_t off = static_cast<size_t>(m) * ctx->sp.ny * ctx->sp.pitch;
+    const size_t off = static_cast<size_t>(m) * ctx->sp.mstride;
     float* dst[3] = {eta, hu, hv};
     for (int i = 0; i < 3; ++i)
         if (dst[i])
@@ -664,12 +660,14 @@ dc_status dc_download_all(dc_ctx* ctx, float* eta, float* hu, float* hv, double*
     DeviceGuard dg_(ctx);
     dc_status st = surface_errors(ctx);
     float* dst[3] = {eta, hu, hv};
-    for (int i = 0; i < 3; ++i)
-        if (dst[i])
-            CU(cudaMemcpy2DAsync(dst[i], ctx->sp.nx * sizeof(float), ctx->f[i],
-                                 ctx->sp.pitch * sizeof(float), ctx->sp.nx * sizeof(float),
-                                 static_cast<size_t>(ctx->sp.ny) * ctx->M, cudaMemcpyDeviceToHost,
-                                 ctx->stream));
+    const size_t cells = static_cast<size_t>(ctx->sp.nx) * ctx->sp.ny;
+    for (int m = 0; m < ctx->M; ++m)
+        for (int i = 0; i < 3; ++i)
+            if (dst[i])
+                CU(cudaMemcpy2DAsync(dst[i] + m * cells, ctx->sp.nx * sizeof(float),
+                                     ctx->f[i] + m * ctx->sp.mstride, ctx->sp.pitch * sizeof(float),
+                                     ctx->sp.nx * sizeof(float), ctx->sp.ny,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
     if (t)
         CU(cudaMemcpyAsync(t, ctx->ctl.t, ctx->M * sizeof(double), cudaMemcpyDeviceToHost,
                            ctx->stream));
@@ -707,10 +705,11 @@ dc_status dc_init_double_jet(dc_ctx* ctx) {
             u[static_cast<size_t>(k) * pitch + j] = static_cast<float>(hu_p[k]);
         }
     const size_t per = static_cast<size_t>(ny) * pitch;
+    const size_t ms = ctx->sp.mstride;
     for (int m = 0; m < ctx->M; ++m) {
-        CU(cudaMemcpyAsync(ctx->f[0] + m * per, e.data(), per * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaMemcpyAsync(ctx->f[1] + m * per, u.data(), per * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
-        CU(cudaMemcpyAsync(ctx->f[2] + m * per, z.data(), per * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->f[0] + m * ms, e.data(), per * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->f[1] + m * ms, u.data(), per * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CU(cudaMemcpyAsync(ctx->f[2] + m * ms, z.data(), per * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
     }
     CU(cudaMemsetAsync(ctx->ctl.t, 0, ctx->M * sizeof(double), ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -740,23 +739,11 @@ dc_status dc_step(dc_ctx* ctx, int32_t n_steps) {
     }
     for (int i = 0; i < n_steps; ++i) {
         const bool scan = ctx->stats != 1;
-        if (ctx->persist) {
-            if (scan) {
-                launch_reset_stats(ctx->stream, ctx->sp, ctx->ctl);
-                launch_cfl_scan(ctx->stream, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
-            }
-            launch_step_begin(ctx->stream, ctx->sp, ctx->ctl, 0ull, 0);
-            launch_step_persistent(ctx->stream, ctx->sp, ctx->exact, ctx->p_grid, ctx->p_nsp,
-                                   ctx->f[0], ctx->f[1], ctx->f[2], ctx->f[3], ctx->f[4],
-                                   ctx->f[5], ctx->ctl);
-            dcg::count_iters_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->ctl.sub, ctx->M,
-                                                                ctx->substep_iters);
-            ctx->launches += (scan ? 2 : 0) + 3;
-        } else if (ctx->use_graph) {
+        if (ctx->use_graph) {
             CU(cudaGraphLaunch(scan ? ctx->step_exec : ctx->step_exec_fused, ctx->stream));
             dcg::count_iters_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->ctl.sub, ctx->M,
                                                                 ctx->substep_iters);
-            ctx->launches += (scan ? 3 : 1) + 1;  // [reset, cfl_scan,] step_begin, count_iters
+            ctx->launches += (scan ? 4 : 2) + 1;  // fix_ghosts, [reset, cfl_scan,] step_begin, count_iters
         } else {
             dc_status st = step_host_loop(ctx, scan);
             if (st) return st;
@@ -778,11 +765,11 @@ dc_status dc_flux_rhs(dc_ctx* ctx, int32_t m, float* d_eta, float* d_hu, float* 
     DeviceGuard dg_(ctx);
     dc_status st = check_member(ctx, m);
     if (st) return st;
-    const size_t per = static_cast<size_t>(ctx->sp.ny) * ctx->sp.pitch;
-    if (!ctx->rhs) CU(cudaMalloc(&ctx->rhs, 3 * per * sizeof(float)));
+    const size_t per = ctx->sp.mstride;
+    if (!ctx->rhs) CU(cudaMalloc(&ctx->rhs, 3 * per * sizeof(float)));  // per = mstride
     // dry-cell check of load() (swe.hpp:319): flux_rhs throws before computing
     std::vector<float> e(static_cast<size_t>(ctx->sp.nx) * ctx->sp.ny);
-    CU(cudaMemcpy2DAsync(e.data(), ctx->sp.nx * sizeof(float), ctx->f[0] + m * per,
+    CU(cudaMemcpy2DAsync(e.data(), ctx->sp.nx * sizeof(float), ctx->f[0] + m * ctx->sp.mstride,
                          ctx->sp.pitch * sizeof(float), ctx->sp.nx * sizeof(float), ctx->sp.ny,
                          cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -799,12 +786,15 @@ dc_status dc_flux_rhs(dc_ctx* ctx, int32_t m, float* d_eta, float* d_hu, float* 
                                    m, j, k);
         return set_err(ctx, DC_EDRY, "flux_rhs: dry cell (non-finite eta)", m);
     }
-    launch_flux_rhs(ctx->stream, ctx->sp, ctx->exact, m, ctx->f[0], ctx->f[1], ctx->f[2],
-                    ctx->rhs, ctx->rhs + per, ctx->rhs + 2 * per, ctx->ctl);
+    fix_ghosts(ctx, ctx->stream);
+    launch_flux_rhs(ctx->stream, ctx->sp, ctx->exact, m, &ctx->maps[0], ctx->f[0], ctx->f[1],
+                    ctx->f[2], ctx->rhs + 2 * ctx->sp.pitch + 2, ctx->rhs + per + 2 * ctx->sp.pitch + 2,
+                    ctx->rhs + 2 * per + 2 * ctx->sp.pitch + 2, ctx->ctl);
+    ctx->launches += 1;
     ctx->launches += 1;
     float* dst[3] = {d_eta, d_hu, d_hv};
     for (int i = 0; i < 3; ++i)
-        CU(cudaMemcpy2DAsync(dst[i], ctx->sp.nx * sizeof(float), ctx->rhs + i * per,
+        CU(cudaMemcpy2DAsync(dst[i], ctx->sp.nx * sizeof(float), ctx->rhs + i * per + 2 * ctx->sp.pitch + 2,
                              ctx->sp.pitch * sizeof(float), ctx->sp.nx * sizeof(float),
                              ctx->sp.ny, cudaMemcpyDeviceToHost, ctx->stream));
     return surface_errors(ctx);
@@ -929,15 +919,15 @@ dc_status dc_set_draw_counter(dc_ctx* ctx, uint64_t d) {
 
 int64_t dc_kernel_launches(dc_ctx* ctx) {
     DeviceGuard dg_(ctx);
-    // graph path: 2 kernels per step + 2 per substep iteration (3 with the separate
-    // substep_end), iterations counted on the device
+    // graph path: 2 kernels per step + 2 per substep iteration, iterations counted on the
+    // device
     unsigned long long iters = 0;
-    if (ctx->use_graph && !ctx->persist && ctx->substep_iters) {  // persistent: 1 per step
+    if (ctx->use_graph && ctx->substep_iters) {
         cudaMemcpyAsync(&iters, ctx->substep_iters, sizeof(iters), cudaMemcpyDeviceToHost,
                         ctx->stream);
         cudaStreamSynchronize(ctx->stream);
     }
-    return ctx->launches + (ctx->fused_end ? 2 : 3) * static_cast<int64_t>(iters);
+    return ctx->launches + 2 * static_cast<int64_t>(iters);
 }
 
 void* dc_stream(dc_ctx* ctx) { return ctx->stream; }
@@ -964,19 +954,17 @@ dc_status dc_time_stages(dc_ctx* ctx, int32_t n_substeps, double* ms_out) {
     cudaStream_t s = ctx->stream;
     std::vector<cudaEvent_t> ev(3 * static_cast<size_t>(n_substeps));
     for (auto& e : ev) CU(cudaEventCreate(&e));
+    fix_ghosts(ctx, s);
     launch_reset_stats(s, ctx->sp, ctx->ctl);
     launch_cfl_scan(s, ctx->sp, ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
     ctx->stats = 2;
     launch_step_begin(s, ctx->sp, ctx->ctl);
     for (int i = 0; i < n_substeps; ++i) {
         CU(cudaEventRecord(ev[3 * i], s));
-        launch_stage(s, ctx->sp, ctx->exact, 1, ctx->f[0], ctx->f[1], ctx->f[2], nullptr, nullptr,
-                     nullptr, ctx->f[3], ctx->f[4], ctx->f[5], ctx->ctl);
+        launch_stage1(ctx, s);
         CU(cudaEventRecord(ev[3 * i + 1], s));
-        launch_stage(s, ctx->sp, ctx->exact, 2, ctx->f[3], ctx->f[4], ctx->f[5], ctx->f[0],
-                     ctx->f[1], ctx->f[2], ctx->f[0], ctx->f[1], ctx->f[2], ctx->ctl);
+        launch_stage2(ctx, s, 0ull, 1);
         CU(cudaEventRecord(ev[3 * i + 2], s));
-        launch_substep_end(s, ctx->sp, ctx->ctl, 0ull, 0);
     }
     CU(cudaStreamSynchronize(s));
     double t1 = 0.0, t2 = 0.0;
@@ -988,7 +976,7 @@ dc_status dc_time_stages(dc_ctx* ctx, int32_t n_substeps, double* ms_out) {
         t2 += b;
     }
     for (auto& e : ev) cudaEventDestroy(e);
-    ctx->launches += 2 + 3 * n_substeps;
+    ctx->launches += 4 + 2 * n_substeps;
     ms_out[0] = t1 / n_substeps;
     ms_out[1] = t2 / n_substeps;
     return surface_errors(ctx);

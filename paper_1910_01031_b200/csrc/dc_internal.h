@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdlib>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <string>
@@ -29,7 +30,12 @@ enum DevErr : int {
 // Constants of the shallow-water stencil, derived exactly as the reference's Stepper
 // derives them (double, then one rounding to float): swe.hpp:277-278,340-344,356-357,380-382.
 struct SweParams {
+    // state layout: every member holds (ny+4) x pitch floats per field -- the ny x nx
+    // cells inside a 2-cell periodic ghost frame (stage kernels read it through TMA);
+    // field pointers address cell (0, 0), cell (k, j) of member m is at
+    // m*mstride + k*pitch + j, k in [-2, ny+2), j in [-2, nx+2)
     int nx, ny, pitch, M;
+    size_t mstride;       // (ny + 4) * pitch
     int by, strips;       // rows per CTA strip, strips per member (uniform strips)
     const int2* units;    // optional CTA row units {m, y0 | y1 << 16}: big strips first,
     int n_units;          // short ones last so the final wave drains quickly (api.cu)
@@ -56,11 +62,6 @@ struct StepCtl {
     int* any_active;    // loop condition (host-visible in the fallback path)
     unsigned* mdone;    // [M] stage-2 CTAs of the member finished this substep (fused end)
     int* n_active;      // members still stepping (fused end: the last one ends the loop)
-    // persistent step (DC_PERSISTENT): work-unit counter and per-member progress
-    unsigned long long* next;  // next work unit to claim
-    unsigned* s1c;      // [M] stage-1 units completed this step (all substeps)
-    int* dsub;          // [M] substep ends published this step (release / acquire)
-    int* hang;          // a dependency wait timed out (scheduling bug guard)
 };
 
 struct ErrParams {
@@ -84,8 +85,6 @@ inline void smem_opt_in(F* func, size_t bytes) {
     const unsigned long long bit = 1ull << (dev & 63);
     if (done.load(std::memory_order_relaxed) & bit) return;
     cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
-    if (const char* c = std::getenv("DC_CARVEOUT"))  // preferred shared-memory carveout, %
-        cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(c));
     done.fetch_or(bit);
 }
 
@@ -112,25 +111,26 @@ void launch_step_begin(cudaStream_t s, const SweParams& sp, StepCtl ctl,
                        unsigned long long cond_handle = 0, int use_cond = 0);
 void launch_reset_stats(cudaStream_t s, const SweParams& sp, StepCtl ctl);
 int swe_stage_occupancy();
-// end_mode of a stage-2 launch: 0 = a separate launch_substep_end follows; 1 = each
-// member's last stage-2 CTA runs the member's substep end (loop flag read by the host);
-// 2 = same, and the CTA that retires the last active member clears the graph's while
-// condition (cond_handle)
-int launch_step_persistent(cudaStream_t s, const SweParams& sp, bool exact, int grid, int nsp,
-                          float* fe, float* fu, float* fv, float* ge, float* gu, float* gv,
-                          StepCtl ctl);
-int swe_persistent_occupancy();
-void launch_stage(cudaStream_t s, const SweParams& sp, bool exact, int stage, const float* ie,
-                  const float* iu, const float* iv, const float* s0e, const float* s0u,
-                  const float* s0v, float* oe, float* ou, float* ov, StepCtl ctl,
+// TMA map of a state set (3 fields field_stride floats apart, origin = storage row -2 of
+// member 0, column -2)
+bool make_state_map(CUtensorMap* map, const float* origin, const SweParams& sp,
+                    size_t field_stride);
+// refresh the ghost frame of a state set (f0 = field 0 at cell (0, 0))
+void launch_fix_ghosts(cudaStream_t s, const SweParams& sp, float* f0, size_t field_stride);
+// One SSP-RK2 stage over every member. maps: [0] the input state set, [1] the psi^n set
+// (stage 2). end_mode of a stage-2 launch:
+// 0 = none; 1 = each member's last stage-2 CTA runs the member's substep end (loop flag
+// read by the host); 2 = same, and the CTA that retires the last active member clears
+// the graph's while condition (cond_handle)
+void launch_stage(cudaStream_t s, const SweParams& sp, bool exact, int stage,
+                  const CUtensorMap* maps, const float* ie, const float* iu, const float* iv,
+                  float* oe, float* ou, float* ov, StepCtl ctl,
                   unsigned long long cond_handle = 0, int end_mode = 0);
-void launch_substep_end(cudaStream_t s, const SweParams& sp, StepCtl ctl,
-                        unsigned long long cond_handle, int use_cond);
 void launch_selftest_math(cudaStream_t s, unsigned long long* counts);
 void launch_cfl_public(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
                        const float* hv, unsigned long long* gmax, int* dry_pos);
-void launch_flux_rhs(cudaStream_t s, const SweParams& sp, bool exact, int m, const float* eta,
-                     const float* hu, const float* hv, float* re, float* ru, float* rv,
-                     StepCtl ctl);
+void launch_flux_rhs(cudaStream_t s, const SweParams& sp, bool exact, int m,
+                     const CUtensorMap* maps, const float* eta, const float* hu, const float* hv,
+                     float* re, float* ru, float* rv, StepCtl ctl);
 
 } // namespace dcg

@@ -73,7 +73,7 @@ __global__ void pf_loglik_kernel(SweParams sp, const float* __restrict__ eta,
         if (threadIdx.x == 0) loglik[m] = -__longlong_as_double(0x7ff0000000000000ll);
         return;
     }
-    const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
+    const size_t mbase = static_cast<size_t>(m) * sp.mstride;
     double* qm = q + static_cast<size_t>(m) * n_obs;
     for (int o = threadIdx.x; o < n_obs; o += blockDim.x) {
         const int j = cells[2 * o], k = cells[2 * o + 1];
@@ -97,8 +97,8 @@ __global__ void resample_fields_kernel(SweParams sp, const int* __restrict__ idx
                                        const float* __restrict__ iv, float* oe, float* ou,
                                        float* ov) {
     const int m = blockIdx.y, k = blockIdx.x;
-    const size_t src = (static_cast<size_t>(idx[m]) * sp.ny + k) * sp.pitch;
-    const size_t dst = (static_cast<size_t>(m) * sp.ny + k) * sp.pitch;
+    const size_t src = static_cast<size_t>(idx[m]) * sp.mstride + static_cast<size_t>(k) * sp.pitch;
+    const size_t dst = static_cast<size_t>(m) * sp.mstride + static_cast<size_t>(k) * sp.pitch;
     for (int j = threadIdx.x; j < sp.nx; j += blockDim.x) {
         oe[dst + j] = ie[src + j];
         ou[dst + j] = iu[src + j];

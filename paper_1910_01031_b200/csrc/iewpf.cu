@@ -74,7 +74,7 @@ __global__ void innovations_kernel(SweParams sp, const float* __restrict__ eta,
                                    double* d, double* sd, double* scal, const int* err) {
     const int m = blockIdx.x;
     if (err[m]) return;
-    const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
+    const size_t mbase = static_cast<size_t>(m) * sp.mstride;
     const double S0 = S[0], S1 = S[1], S2 = S[2], S3 = S[3];
     for (int o = threadIdx.x; o < n_obs; o += blockDim.x) {
         const int j = cells[2 * o], k = cells[2 * o + 1];
@@ -256,7 +256,7 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
     const int j0 = (tl % tiles_x) * TX, k0 = (tl / tiles_x) * TY;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const int j = j0 + tx;
-    const size_t mbase = static_cast<size_t>(m) * sp.ny * sp.pitch;
+    const size_t mbase = static_cast<size_t>(m) * sp.mstride;
     // each thread stages (and later owns) its cells in shared memory: registers stay free
     // for occupancy, and no barrier is needed since only the owner touches them
 #pragma unroll
@@ -595,7 +595,7 @@ __global__ void drifters_kernel(SweParams sp, const float* __restrict__ eta,
         atomicCAS(err + m, 0, E_DRY_DRIFTER);
         return;
     }
-    const size_t c = static_cast<size_t>(m) * sp.ny * sp.pitch + static_cast<size_t>(k) * sp.pitch + j;
+    const size_t c = static_cast<size_t>(m) * sp.mstride + static_cast<size_t>(k) * sp.pitch + j;
     const double h = sp.h_eq + static_cast<double>(eta[c]);
     if (!(h > 0.0)) {
         atomicCAS(err + m, 0, E_DRY_DRIFTER);
@@ -630,7 +630,7 @@ __global__ void observe_mooring_kernel(SweParams sp, const float* __restrict__ e
         atomicExch(bad, 1);
         return;
     }
-    const size_t c = static_cast<size_t>(m) * sp.ny * sp.pitch + static_cast<size_t>(k) * sp.pitch + j;
+    const size_t c = static_cast<size_t>(m) * sp.mstride + static_cast<size_t>(k) * sp.pitch + j;
     const double h = sp.h_eq + static_cast<double>(eta[c]);
     y[2 * o] = static_cast<double>(hu[c]) * sp.h_eq / h;
     y[2 * o + 1] = static_cast<double>(hv[c]) * sp.h_eq / h;

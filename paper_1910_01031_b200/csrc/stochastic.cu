@@ -166,7 +166,7 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
     const int j = j0 + tx;
     const size_t pitch = sp.pitch;
     // this thread's cells: column j, rows k0 + ty + 8q
-    const size_t cell0 = static_cast<size_t>(m) * sp.ny * pitch + static_cast<size_t>(k0 + ty) * pitch + j;
+    const size_t cell0 = static_cast<size_t>(m) * sp.mstride + static_cast<size_t>(k0 + ty) * pitch + j;
     const size_t step = static_cast<size_t>(kWarps) * pitch;
     bool okq[kRowsPerThread];
 #pragma unroll
