@@ -36,7 +36,8 @@ typedef enum dc_status {
     DC_ECUDA = 6,      /* CUDA runtime failure */
     DC_ESTATE = 7,     /* API misuse (bad member index, wrong call order) */
     DC_EIO = 8,        /* std::runtime_error from snapshot / file I/O (state.hpp:71-116) */
-    DC_ECOLLAPSE = 9   /* standard PF weights: every weight underflows */
+    DC_ECOLLAPSE = 9,  /* standard PF weights: every weight underflows */
+    DC_ENCCL = 10      /* NCCL failure (multi-GPU communicator, dc_comm_*) */
 } dc_status;
 
 /* Parameter block: ModelGrid + PhysParams + SchemeParams + ErrorParams + seed. */
@@ -145,10 +146,15 @@ dc_status dc_drifters_advect(dc_ctx* ctx, double dt);
 dc_status dc_drifters_get(dc_ctx* ctx, double* pos, int32_t* wind);
 /* number of drifter copies per member (DC_ESTATE when none are set). */
 dc_status dc_drifters_count(dc_ctx* ctx, int32_t* n_d);
+/* restore positions and winding counts [n_members][n_d][2] (checkpoint resume). */
+dc_status dc_drifters_restore(dc_ctx* ctx, const double* pos, const int32_t* wind, int32_t n_d);
 
 /* ---- snapshots and checkpoints (state.hpp:43-116) ----------- */
 /* The context's parameters and member slice. */
 dc_status dc_get_config(dc_ctx* ctx, dc_config* cfg, int32_t* n_members, int64_t* member_base);
+/* the model-error stream tag (dc_set_model_error_tag) and IEWPF mode (dc_iewpf_set_mode). */
+dc_status dc_get_model_error_tag(dc_ctx* ctx, uint64_t* tag);
+dc_status dc_iewpf_get_mode(dc_ctx* ctx, int32_t* mode);
 /* save_snapshot (state.hpp:71-85) of member m to a file: "DCST" | u32 version 1 | u32 nx |
  * u32 ny | f64 t | eta f32[nx*ny] | hu | hv, little endian, byte-identical to the
  * reference writer. Synchronous. */
@@ -158,10 +164,13 @@ dc_status dc_save_snapshot(dc_ctx* ctx, int32_t m, const char* path);
  * extents must equal the context grid (DC_EINVAL otherwise). Synchronous. */
 dc_status dc_load_snapshot(dc_ctx* ctx, int32_t m, const char* path);
 /* Checkpoint directory (SPEC.md ensemble_engine External Interfaces):
- * dir/ensemble/particle_<i>.dcst for every member (global id i), dir/rng_state.txt (master
- * seed, model-error draw counter, filter cycle: the whole counter-based RNG state) and
- * dir/meta.txt (parameter echo). The directory and dir/ensemble are created if absent.
- * Restoring reproduces the uninterrupted run bit for bit. */
+ * dir/ensemble/particle_<i>.dcst for every member (global id i), when drifter copies are
+ * set dir/ensemble/particle_<i>.drifters ("drifter,x,y,wind_x,wind_y" per line, %.17g),
+ * dir/rng_state_<first id>.txt (master seed, model-error draw counter and stream tag,
+ * filter cycle, IEWPF mode: the whole counter-based RNG and filter state of the slice)
+ * and dir/meta.txt (parameter echo). The directory and dir/ensemble are created if absent.
+ * Restoring reproduces the uninterrupted run bit for bit, drifters
+ * included; load also accepts the single-context name dir/rng_state.txt. */
 dc_status dc_checkpoint_save(dc_ctx* ctx, const char* dir, uint64_t filter_cycle);
 dc_status dc_checkpoint_load(dc_ctx* ctx, const char* dir, uint64_t* filter_cycle);
 
@@ -311,6 +320,25 @@ dc_status dc_readback_wait(dc_ctx* ctx, int32_t slot, dc_particle_diag* per_memb
 dc_status dc_da_cycle(dc_ctx* ctx, int32_t n_steps, const dc_obs* obs, int32_t n_obs,
                       const double* S, const double* usig, uint64_t cycle);
 
+/* ---- multi-GPU: one process / context per GPU, NCCL over NVLink ---- */
+/* Ranks hold contiguous particle ranges in rank order (dc_create's member_base); the
+ * host driver creates one NCCL id on rank 0 (dc_comm_unique_id), broadcasts its 128
+ * bytes to every rank (MPI_Bcast, a shared file, torch.distributed, ...) and each rank
+ * attaches its context (collective: blocks until all ranks joined; checks the partition
+ * covers [0, n_total)). While attached, dc_iewpf_assimilate / dc_da_cycle exchange the
+ * (c_i, zeta_i) pairs of all ranks at the IEWPF barrier, and dc_forecast_error /
+ * dc_readback_enqueue(FORECAST_ERROR) gather every rank's drifter ensemble to rank 0
+ * (the other ranks report no statistics: NaN / untouched) -- NCCL send/recv on the
+ * context stream, no host synchronisation. Results are bitwise independent of the
+ * number of ranks. NCCL is loaded at run time (libnccl.so.2); failures -> DC_ENCCL.
+ * Replaces: the spec's worker-pool barrier. */
+#define DC_COMM_ID_BYTES 128
+dc_status dc_comm_unique_id(uint8_t* id_out);
+dc_status dc_comm_attach(dc_ctx* ctx, const uint8_t* id, int32_t rank, int32_t world,
+                         int64_t n_total);
+dc_status dc_comm_detach(dc_ctx* ctx);
+dc_status dc_comm_info(dc_ctx* ctx, int32_t* rank, int32_t* world, int64_t* n_total);
+
 /* ---- instrumentation ------------------------------------------------------------ */
 /* number of kernels this context has launched (host-side counter). */
 int64_t dc_kernel_launches(dc_ctx* ctx);
@@ -321,6 +349,20 @@ dc_status dc_counters(dc_ctx* ctx, uint64_t* out);
  * events around each stage kernel; ms_out[0..1] = mean stage-1 / stage-2 duration.
  * Advances the state (n_substeps substeps of a model step). */
 dc_status dc_time_stages(dc_ctx* ctx, int32_t n_substeps, double* ms_out);
+/* Per-kernel profile of everything the calling thread launches between begin and end
+ * (any context): each kernel is bracketed by CUDA events on its own stream, and its
+ * algorithmic HBM bytes (the data it must read and write once) are
+ * accumulated per kernel name. Inside the window dc_step runs its host-driven substep
+ * loop, so the stage kernels are timed individually. dc_profile_end synchronises and
+ * writes up to cap entries (first-launch order); *n_out = number of distinct kernels. */
+typedef struct dc_kernel_time {
+    char name[40];
+    int64_t launches;
+    double ms;     /* summed device time of the launches */
+    double bytes;  /* summed algorithmic bytes of the launches */
+} dc_kernel_time;
+dc_status dc_profile_begin(dc_ctx* ctx);
+dc_status dc_profile_end(dc_ctx* ctx, dc_kernel_time* out, int32_t cap, int32_t* n_out);
 /* the cudaStream_t the context runs on. */
 void* dc_stream(dc_ctx* ctx);
 /* Exhaustive device self-check of the branch-free IEEE sqrt / reciprocal used by the

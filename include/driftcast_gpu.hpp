@@ -7,6 +7,7 @@
 // thrown, so existing catch sites keep working unchanged.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -42,6 +43,7 @@ inline void throw_status(dc_status st, const std::string& msg) {
     case DC_ERUNAWAY:
     case DC_EIO:        // snapshot / file I/O (state.hpp:71-116 throws runtime_error)
     case DC_ECOLLAPSE:  // standard PF weights: "ensemble collapse"
+    case DC_ENCCL:      // multi-GPU communicator
         throw std::runtime_error(msg);
     default: throw std::runtime_error("driftcast_gpu: " + msg);
     }
@@ -129,11 +131,82 @@ public:
         check(dc_iewpf_assimilate(ctx_, obs.data(), static_cast<int>(obs.size()), f.S,
                                   f.usig.data(), cycle));
     }
+    // the analysis split at its barrier (multi-GPU drivers that run their own collective):
+    // begin -> exchange every rank's (c_i, zeta_i) [n_total][2] -> finish
+    void iewpf_begin(const std::vector<dc_obs>& obs, const FilterOperators& f,
+                     std::uint64_t cycle, int n_total, double* cz_out, bool cz_on_device) {
+        check(dc_iewpf_begin(ctx_, obs.data(), static_cast<int>(obs.size()), f.S, f.usig.data(),
+                             cycle, n_total, cz_out, cz_on_device ? 1 : 0));
+    }
+    void iewpf_finish(const double* cz_all, bool cz_on_device) {
+        check(dc_iewpf_finish(ctx_, cz_all, cz_on_device ? 1 : 0));
+    }
+    // the original one-stage IEWPF instead of the two-stage default
+    void set_one_stage(bool one_stage) {
+        check(dc_iewpf_set_mode(ctx_, one_stage ? DC_IEWPF_ONE_STAGE : DC_IEWPF_TWO_STAGE));
+    }
+    // multi-GPU (one process per GPU): join the ranks' NCCL communicator; afterwards
+    // iewpf_assimilate / da_cycle exchange (c_i, zeta_i) at the barrier and forecast
+    // statistics gather every rank's drifters to rank 0
+    void comm_attach(const std::uint8_t* nccl_id, int rank, int world, std::int64_t n_total) {
+        check(dc_comm_attach(ctx_, nccl_id, rank, world, n_total));
+    }
+    void comm_detach() { check(dc_comm_detach(ctx_)); }
     // one DA cycle
     void da_cycle(int n_steps, const std::vector<dc_obs>& obs, const FilterOperators& f,
                   std::uint64_t cycle) {
         check(dc_da_cycle(ctx_, n_steps, obs.data(), static_cast<int>(obs.size()), f.S,
                           f.usig.data(), cycle));
+    }
+    // innovation of every member: d[m][o][2] (synchronous)
+    std::vector<double> innovations(const std::vector<dc_obs>& obs) {
+        std::vector<double> d(static_cast<size_t>(n_) * obs.size() * 2);
+        check(dc_innovations(ctx_, obs.data(), static_cast<int>(obs.size()), d.data()));
+        return d;
+    }
+    // observe_mooring without noise on member m: y[o][2]
+    std::vector<double> observe_mooring(int m, const std::vector<double>& xy) {
+        std::vector<double> y(xy.size());
+        check(dc_observe_mooring(ctx_, m, xy.data(), static_cast<int>(xy.size() / 2), y.data()));
+        return y;
+    }
+    // Stepper::flux_rhs (swe.hpp:229-239) of member m, Field2D layout
+    void flux_rhs(int m, std::vector<float>& de, std::vector<float>& du, std::vector<float>& dv) {
+        const size_t n = static_cast<size_t>(cfg_.nx) * cfg_.ny;
+        de.resize(n);
+        du.resize(n);
+        dv.resize(n);
+        check(dc_flux_rhs(ctx_, m, de.data(), du.data(), dv.data()));
+    }
+    // Stepper::cfl_dt (swe.hpp:212-226) of every member
+    std::vector<double> cfl_dt() {
+        std::vector<double> dt(n_);
+        check(dc_cfl_dt(ctx_, dt.data()));
+        return dt;
+    }
+    // pipelined per-cycle outputs: enqueue behind the queued work, read while the next
+    // cycle runs (slot 0 or 1); truth_xy [n_d][2] enables the forecast statistics
+    void readback_enqueue(int slot, const std::vector<double>* truth_xy) {
+        int what = DC_READBACK_DIAG | DC_READBACK_DRIFTERS;
+        if (truth_xy) what |= DC_READBACK_FORECAST_ERROR;
+        check(dc_readback_enqueue(ctx_, slot, what, truth_xy ? truth_xy->data() : nullptr));
+    }
+    struct Readback {
+        std::vector<dc_particle_diag> diag;
+        double w_beta[2] = {0.0, 0.0};
+        std::vector<double> pos;
+        std::vector<std::int32_t> wind;
+        double E = 0.0, RMSE = 0.0;
+    };
+    Readback readback_wait(int slot, int n_drifters) {
+        Readback r;
+        r.diag.resize(n_);
+        r.pos.resize(static_cast<size_t>(n_) * n_drifters * 2);
+        r.wind.resize(r.pos.size());
+        r.E = r.RMSE = std::nan("");
+        check(dc_readback_wait(ctx_, slot, r.diag.data(), r.w_beta, r.pos.data(), r.wind.data(),
+                               &r.E, &r.RMSE));
+        return r;
     }
     std::vector<dc_particle_diag> diagnostics(double* w_beta = nullptr) {
         std::vector<dc_particle_diag> d(n_);

@@ -15,13 +15,13 @@ LIB_PATH = os.environ.get("DC_LIB_PATH") or os.path.join(HERE, "libdriftcast_gpu
 HEADER = os.path.join(os.path.dirname(HERE), "include", "driftcast_gpu.h")
 
 (DC_OK, DC_EINVAL, DC_EDRY, DC_ENONFINITE, DC_ERUNAWAY, DC_EALIGN, DC_ECUDA, DC_ESTATE, DC_EIO,
- DC_ECOLLAPSE) = range(10)
+ DC_ECOLLAPSE, DC_ENCCL) = range(11)
 DC_NOISE_PHILOX, DC_NOISE_INJECTED = 0, 1
 
 STATUS_NAMES = {
     DC_OK: "DC_OK", DC_EINVAL: "DC_EINVAL", DC_EDRY: "DC_EDRY", DC_ENONFINITE: "DC_ENONFINITE",
     DC_ERUNAWAY: "DC_ERUNAWAY", DC_EALIGN: "DC_EALIGN", DC_ECUDA: "DC_ECUDA",
-    DC_ESTATE: "DC_ESTATE", DC_EIO: "DC_EIO", DC_ECOLLAPSE: "DC_ECOLLAPSE",
+    DC_ESTATE: "DC_ESTATE", DC_EIO: "DC_EIO", DC_ECOLLAPSE: "DC_ECOLLAPSE", DC_ENCCL: "DC_ENCCL",
 }
 
 
@@ -58,6 +58,13 @@ class DcTruthPlan(C.Structure):
                 ("r_hu", C.c_double), ("r_hv", C.c_double)]
 
 
+class DcKernelTime(C.Structure):
+    """dc_kernel_time: one kernel of a dc_profile_begin / dc_profile_end window."""
+
+    _fields_ = [("name", C.c_char * 40), ("launches", C.c_int64), ("ms", C.c_double),
+                ("bytes", C.c_double)]
+
+
 class DcParticleDiag(C.Structure):
     _fields_ = [("c", C.c_double), ("phi", C.c_double), ("gamma", C.c_double),
                 ("zeta", C.c_double), ("alpha", C.c_double)]
@@ -80,7 +87,9 @@ EXPORTS = [
     "dc_set_model_error_tag", "dc_generate_truth", "dc_iewpf_set_mode",
     "dc_iewpf_diagnostics_write", "dc_drifters_get_device", "dc_forecast_error_gathered",
     "dc_readback_enqueue", "dc_readback_wait", "dc_member_bytes", "dc_member_export",
-    "dc_member_import",
+    "dc_member_import", "dc_profile_begin", "dc_profile_end", "dc_comm_unique_id",
+    "dc_comm_attach", "dc_comm_detach", "dc_comm_info", "dc_drifters_restore",
+    "dc_get_model_error_tag", "dc_iewpf_get_mode",
 ]
 
 
@@ -145,6 +154,15 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "dc_selftest_math": (st, [C.c_int32, C.POINTER(C.c_uint64)]),
         "dc_counters": (st, [vp, C.POINTER(C.c_uint64)]),
         "dc_time_stages": (st, [vp, C.c_int32, dp]),
+        "dc_profile_begin": (st, [vp]),
+        "dc_comm_unique_id": (st, [C.POINTER(C.c_uint8)]),
+        "dc_comm_attach": (st, [vp, C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int64]),
+        "dc_comm_detach": (st, [vp]),
+        "dc_drifters_restore": (st, [vp, dp, ip, C.c_int32]),
+        "dc_get_model_error_tag": (st, [vp, C.POINTER(C.c_uint64)]),
+        "dc_iewpf_get_mode": (st, [vp, ip]),
+        "dc_comm_info": (st, [vp, ip, ip, C.POINTER(C.c_int64)]),
+        "dc_profile_end": (st, [vp, C.POINTER(DcKernelTime), C.c_int32, ip]),
         "dc_drifters_count": (st, [vp, ip]),
         "dc_get_config": (st, [vp, cfgp, ip, C.POINTER(C.c_int64)]),
         "dc_save_snapshot": (st, [vp, C.c_int32, C.c_char_p]),

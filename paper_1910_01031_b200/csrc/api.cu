@@ -1,6 +1,7 @@
 // api.cu -- the C ABI (include/driftcast_gpu.h): ensemble context, device memory,
 // the device-side substep loop as a CUDA graph with a while-node, error surfacing.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -18,6 +19,17 @@
 #include "iewpf_host.h"
 
 using namespace dcg;
+
+// NCCL communicator + partition of a multi-GPU context (dc_comm_attach, comm_api.inc)
+struct CommState {
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+    int64_t n_total = 0;
+    std::vector<int64_t> base;  // [world + 1]: first global particle id of each rank
+    double* gpos = nullptr;     // rank 0: every member's drifters, id order [n_total][n_d][2]
+    int* gwind = nullptr;
+    size_t gcap = 0;            // members x drifters the gather buffers hold
+};
 
 struct dc_ctx {
     dc_config cfg{};
@@ -61,6 +73,7 @@ struct dc_ctx {
     IewpfBuffers iw{};
     FeScratch fe{};  // forecast_error scratch
     ReadbackSlot rb[kReadbackSlots];  // pipelined per-cycle outputs
+    CommState* comm = nullptr;        // dc_comm_attach (multi-GPU), else single context
     // error reporting
     std::string err;
     int em = -1, ej = -1, ek = -1, esub = -1;
@@ -89,6 +102,12 @@ struct DeviceGuard {
 };
 
 namespace {
+
+// comm_api.inc (included at the end of this file)
+void comm_free(dc_ctx* ctx);
+dc_status iewpf_assimilate_comm(dc_ctx* ctx, const dc_obs* obs, int32_t n_obs, const double* S,
+                                const double* usig, uint64_t cycle);
+dc_status comm_gather_drifters(dc_ctx* ctx);
 
 const char* kVersion = "driftcast-b200 0.1 (sm_100a)";
 
@@ -238,6 +257,18 @@ dc_status check_member(dc_ctx* ctx, int m) {
     return DC_OK;
 }
 
+// A member whose state is overwritten (upload, init, snapshot / checkpoint load, import)
+// starts healthy: its device error flags are cleared. The reference throws per call and
+// never poisons a particle, so a failed member must be recoverable by reloading it.
+dc_status clear_member_errors(dc_ctx* ctx, int m0, int n) {
+    cudaStream_t s = ctx->stream;
+    CU(cudaMemsetAsync(ctx->ctl.err + m0, 0, n * sizeof(int), s));
+    CU(cudaMemsetAsync(ctx->ctl.err_sub + m0, 0, n * sizeof(int), s));
+    const std::vector<int> big(n, 0x7fffffff);  // pageable: staged before the call returns
+    CU(cudaMemcpyAsync(ctx->ctl.err_pos + m0, big.data(), n * sizeof(int), cudaMemcpyHostToDevice, s));
+    return DC_OK;
+}
+
 // The two stages of one substep: psi^n (set 0) -> psi* (set 1) -> psi^n+1 (set 0).
 void launch_stage1(dc_ctx* ctx, cudaStream_t s) {
     const CUtensorMap maps[2] = {ctx->maps[0], ctx->maps[0]};
@@ -330,6 +361,7 @@ dc_status step_host_loop(dc_ctx* ctx, bool with_scan) {
         guess = 1;
     }
     ctx->last_max_sub = std::max(1, done);
+    KScope ks(s, "count_iters", 4.0 * ctx->M);
     count_iters_kernel<<<1, 1024, 0, s>>>(ctx->ctl.sub, ctx->M, ctx->host_iters);
     ctx->launches += 1;
     return DC_OK;
@@ -337,14 +369,15 @@ dc_status step_host_loop(dc_ctx* ctx, bool with_scan) {
 
 // q_half_apply on ctx->corr with the CFL statistics of the result fused in (the
 // accumulators are reset first unless they already are).
-void apply_q_half_with_stats(dc_ctx* ctx, const int* offsets, double scale) {
+void apply_q_half_with_stats(dc_ctx* ctx, const int* offsets, double scale,
+                             const char* prof_name = "q_half_apply") {
     if (ctx->stats != 0) {
         launch_reset_stats(ctx->stream, ctx->sp, ctx->ctl);
         ctx->launches += 1;
     }
     launch_q_half_apply(ctx->stream, ctx->sp, ctx->ep, ctx->corr, offsets, scale, ctx->f[0],
                         ctx->f[1], ctx->f[2], ctx->ctl.err, ctx->ctl.err_pos, ctx->M,
-                        ctx->ctl.mx);
+                        ctx->ctl.mx, prof_name);
     ctx->stats = 1;
 }
 
@@ -583,6 +616,7 @@ dc_status dc_destroy(dc_ctx* ctx) {
     iewpf_free(ctx->iw);
     fe_free(ctx->fe);
     readback_free(ctx->rb);
+    comm_free(ctx);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return DC_OK;
@@ -613,6 +647,7 @@ dc_status dc_upload_member(dc_ctx* ctx, int32_t m, const float* eta, const float
                              ctx->sp.nx * sizeof(float), ctx->sp.nx * sizeof(float), ctx->sp.ny,
                              cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaMemcpyAsync(ctx->ctl.t + m, &t, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    if ((st = clear_member_errors(ctx, m, 1))) return st;
     CU(cudaStreamSynchronize(ctx->stream)); // t is a stack value
     ctx->stats = 2;
     return DC_OK;
@@ -633,7 +668,7 @@ dc_status dc_upload_all(dc_ctx* ctx, const float* eta, const float* hu, const fl
         CU(cudaMemcpyAsync(ctx->ctl.t, t, ctx->M * sizeof(double), cudaMemcpyHostToDevice,
                            ctx->stream));
     ctx->stats = 2;
-    return DC_OK;
+    return clear_member_errors(ctx, 0, ctx->M);
 }
 
 dc_status dc_download_member(dc_ctx* ctx, int32_t m, float* eta, float* hu, float* hv,
@@ -712,6 +747,8 @@ dc_status dc_init_double_jet(dc_ctx* ctx) {
         CU(cudaMemcpyAsync(ctx->f[2] + m * ms, z.data(), per * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
     }
     CU(cudaMemsetAsync(ctx->ctl.t, 0, ctx->M * sizeof(double), ctx->stream));
+    dc_status st = clear_member_errors(ctx, 0, ctx->M);
+    if (st) return st;
     CU(cudaStreamSynchronize(ctx->stream));
     ctx->stats = 2;
     return DC_OK;
@@ -739,7 +776,8 @@ dc_status dc_step(dc_ctx* ctx, int32_t n_steps) {
     }
     for (int i = 0; i < n_steps; ++i) {
         const bool scan = ctx->stats != 1;
-        if (ctx->use_graph) {
+        // inside a profile window the stage kernels are launched (and timed) one by one
+        if (ctx->use_graph && !kprof_active()) {
             CU(cudaGraphLaunch(scan ? ctx->step_exec : ctx->step_exec_fused, ctx->stream));
             dcg::count_iters_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->ctl.sub, ctx->M,
                                                                 ctx->substep_iters);
@@ -911,6 +949,18 @@ dc_status dc_set_model_error_tag(dc_ctx* ctx, uint64_t tag) {
     return DC_OK;
 }
 
+dc_status dc_get_model_error_tag(dc_ctx* ctx, uint64_t* tag) {
+    if (!ctx || !tag) return DC_ESTATE;
+    *tag = ctx->me_tag;
+    return DC_OK;
+}
+
+dc_status dc_iewpf_get_mode(dc_ctx* ctx, int32_t* mode) {
+    if (!ctx || !mode) return DC_ESTATE;
+    *mode = ctx->iw.one_stage ? DC_IEWPF_ONE_STAGE : DC_IEWPF_TWO_STAGE;
+    return DC_OK;
+}
+
 dc_status dc_set_draw_counter(dc_ctx* ctx, uint64_t d) {
     DeviceGuard dg_(ctx);
     ctx->me_draw = d;
@@ -982,6 +1032,20 @@ dc_status dc_time_stages(dc_ctx* ctx, int32_t n_substeps, double* ms_out) {
     return surface_errors(ctx);
 }
 
+dc_status dc_profile_begin(dc_ctx* ctx) {
+    if (!ctx) return DC_ESTATE;
+    kprof_begin();
+    return DC_OK;
+}
+
+dc_status dc_profile_end(dc_ctx* ctx, dc_kernel_time* out, int32_t cap, int32_t* n_out) {
+    DeviceGuard dg_(ctx);
+    if (!ctx) return DC_ESTATE;
+    const int n = kprof_end(out, cap);
+    if (n_out) *n_out = n;
+    return surface_errors(ctx);
+}
+
 dc_status dc_selftest_math(int32_t device, uint64_t* counts) {
     if (cudaSetDevice(device) != cudaSuccess) return DC_ECUDA;
     unsigned long long* d = nullptr;
@@ -998,3 +1062,4 @@ dc_status dc_selftest_math(int32_t device, uint64_t* counts) {
 // IEWPF / observation entry points live in iewpf_api.cu; they need the context layout.
 #include "iewpf_api.inc"
 #include "experiment_api.inc"
+#include "comm_api.inc"

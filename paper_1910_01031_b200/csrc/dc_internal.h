@@ -88,6 +88,22 @@ inline void smem_opt_in(F* func, size_t bytes) {
     done.fetch_or(bit);
 }
 
+// ---- kernel profiler (kprof.cu; dc_profile_begin / dc_profile_end) ----
+// A launcher declares `KScope ks(stream, "kernel", algorithmic_bytes);` before its launch:
+// inside an open profile window (and outside stream capture) the kernel is bracketed by
+// CUDA events on its stream; otherwise the scope costs one pointer test.
+struct KScope {
+    KScope(cudaStream_t s, const char* name, double bytes);
+    ~KScope();
+    KScope(const KScope&) = delete;
+    KScope& operator=(const KScope&) = delete;
+    cudaStream_t s;
+    int rec;
+};
+bool kprof_active();
+void kprof_begin();
+int kprof_end(dc_kernel_time* out, int cap);
+
 // stochastic.cu launchers
 void launch_philox_noise(cudaStream_t s, const ErrParams& ep, int M, uint64_t seed, uint64_t tag,
                          int64_t member_base, uint32_t substream, uint64_t draw, double* xi,
@@ -102,7 +118,7 @@ void launch_coarse_soar(cudaStream_t s, const ErrParams& ep, int M, const double
 void launch_q_half_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
                          const double* corr, const int* offsets, double scale, float* eta,
                          float* hu, float* hv, int* err, int* err_pos, int M,
-                         unsigned* mx = nullptr);
+                         unsigned* mx = nullptr, const char* prof_name = "q_half_apply");
 
 // swe.cu launchers
 void launch_cfl_scan(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,

@@ -110,9 +110,16 @@ __global__ void resample_fields_kernel(SweParams sp, const int* __restrict__ idx
 __global__ void resample_members_kernel(int M, int n_d, const int* __restrict__ idx,
                                         const double* __restrict__ t_in, double* t_out,
                                         const double* __restrict__ pos_in, double* pos_out,
-                                        const int* __restrict__ wind_in, int* wind_out) {
+                                        const int* __restrict__ wind_in, int* wind_out,
+                                        const int* __restrict__ err_old, int* err, int* err_pos,
+                                        int* err_sub) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < M) t_out[i] = t_in[idx[i]];
+    if (i < M) {
+        t_out[i] = t_in[idx[i]];
+        err[i] = err_old[idx[i]];
+        err_pos[i] = err_old[M + idx[i]];
+        err_sub[i] = err_old[2 * M + idx[i]];
+    }
     if (n_d > 0 && i < M * n_d * 2) {
         const int m = i / (n_d * 2), r = i - m * n_d * 2;
         const size_t src = static_cast<size_t>(idx[m]) * n_d * 2 + r;
@@ -195,18 +202,21 @@ forecast_error_kernel(SweParams sp, int M, int n_d, const double* __restrict__ p
 
 void launch_obs_noise(cudaStream_t s, uint64_t seed, int kind, const int* ids, int n,
                       uint64_t obs_index, double sr_hu, double sr_hv, double* eps) {
+    KScope ks(s, "obs_noise", 20.0 * n);
     obs_noise_kernel<<<(n + 127) / 128, 128, 0, s>>>(seed, kind, ids, n, obs_index, sr_hu, sr_hv,
                                                      eps);
 }
 
 void launch_observe_drifters(cudaStream_t s, const SweParams& sp, const double* prev,
                              const double* cur, int n, double dt_obs, const double* eps, double* y) {
+    KScope ks(s, "observe_drifters", 64.0 * n);
     observe_drifters_kernel<<<(n + 127) / 128, 128, 0, s>>>(sp, prev, cur, n, dt_obs, eps, y);
 }
 
 void launch_pf_loglik(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
                       const float* hv, const double* obs, const int* cells, int n_obs, double r_hu,
                       double r_hv, double* q, double* loglik, const int* err, int M) {
+    KScope ks(s, "pf_loglik", (12.0 + 16.0) * n_obs * M);
     pf_loglik_kernel<<<M, 128, 0, s>>>(sp, eta, hu, hv, obs, cells, n_obs, r_hu, r_hv, q, loglik,
                                        err);
 }
@@ -214,15 +224,22 @@ void launch_pf_loglik(cudaStream_t s, const SweParams& sp, const float* eta, con
 void launch_resample(cudaStream_t s, const SweParams& sp, int M, const int* idx, const float* ie,
                      const float* iu, const float* iv, float* oe, float* ou, float* ov,
                      const double* t_in, double* t_out, int n_d, const double* pos_in,
-                     double* pos_out, const int* wind_in, int* wind_out) {
-    resample_fields_kernel<<<dim3(sp.ny, M), 128, 0, s>>>(sp, idx, ie, iu, iv, oe, ou, ov);
+                     double* pos_out, const int* wind_in, int* wind_out, const int* err_old,
+                     int* err, int* err_pos, int* err_sub) {
+    {
+        KScope ks(s, "resample_fields", 24.0 * sp.nx * sp.ny * M);
+        resample_fields_kernel<<<dim3(sp.ny, M), 128, 0, s>>>(sp, idx, ie, iu, iv, oe, ou, ov);
+    }
+    KScope ks(s, "resample_members", (16.0 + 48.0 * n_d) * M);
     const int n = (M * n_d * 2 > M) ? M * n_d * 2 : M;
     resample_members_kernel<<<(n + 127) / 128, 128, 0, s>>>(M, n_d, idx, t_in, t_out, pos_in,
-                                                            pos_out, wind_in, wind_out);
+                                                            pos_out, wind_in, wind_out, err_old,
+                                                            err, err_pos, err_sub);
 }
 
 void launch_forecast_error(cudaStream_t s, const SweParams& sp, int M, int n_d, const double* pos,
                            const int* wind, const double* truth, double* ed, double* rd) {
+    KScope ks(s, "forecast_error", 24.0 * n_d * M + 32.0 * n_d);
     forecast_error_kernel<<<n_d, kFeThreads, 0, s>>>(sp, M, n_d, pos, wind, truth, ed, rd);
 }
 

@@ -640,6 +640,7 @@ __global__ void observe_mooring_kernel(SweParams sp, const float* __restrict__ e
 
 void launch_obs_locate(cudaStream_t s, const SweParams& sp, const double* obs, int n_obs,
                        int* cells, int* bad) {
+    KScope ks(s, "obs_locate", 40.0 * n_obs);
     obs_locate_kernel<<<(n_obs + 127) / 128, 128, 0, s>>>(sp, obs, n_obs, cells, bad);
 }
 
@@ -647,12 +648,15 @@ void launch_innovations(cudaStream_t s, const SweParams& sp, const float* eta, c
                         const float* hv, const double* obs, const int* cells, int n_obs,
                         const double* S, double log_ne, double* d, double* sd, double* scal,
                         const int* err, int M) {
+    // per (member, obs): a 12 B state gather, d and S d written (32 B)
+    KScope ks(s, "innovations", 44.0 * n_obs * M + 40.0 * n_obs);
     innovations_kernel<<<M, 256, 0, s>>>(sp, eta, hu, hv, obs, cells, n_obs, S, log_ne, d, sd,
                                           scal, err);
 }
 
 void launch_pull_windows(cudaStream_t s, const ErrParams& ep, const double* sd, int n_obs,
                          double* win, const int* err, int M) {
+    KScope ks(s, "pull_windows", (16.0 + 8.0 * WIN * WIN) * n_obs * M);
     pull_windows_kernel<<<dim3(n_obs, M), 128, 0, s>>>(ep, sd, n_obs, win, err);
 }
 
@@ -660,6 +664,7 @@ void launch_tile_lists(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
                        int n_obs, int* lists, int* counts, int* n_tiles_out, int* tiles_x_out) {
     const int tiles_x = (sp.nx + TX - 1) / TX, tiles_y = (sp.ny + TY - 1) / TY;
     const int n_tiles = tiles_x * tiles_y;
+    KScope ks(s, "tile_lists", 16.0 * n_tiles * n_obs + 8.0 * n_obs);
     tile_lists_kernel<<<(n_tiles * 32 + 127) / 128, 128, 0, s>>>(
         sp, ep, cells, n_obs, tiles_x, n_tiles, reinterpret_cast<int4*>(lists), counts);
     *n_tiles_out = n_tiles;
@@ -671,10 +676,17 @@ size_t pull_table_bytes() { return sizeof(tile::TabA); }
 void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep, const double* win,
                        const int* cells, int n_obs, const int* lists, const int* counts,
                        int n_tiles, int tiles_x, void* tabs, float* eta, float* hu, float* hv,
-                       int* err, int* err_pos, int M) {
+                       int* err, int* err_pos, int M, double entries, double touched_cells) {
     tile::TabA* T = static_cast<tile::TabA*>(tabs);
-    pull_tables_kernel<<<dim3(n_tiles, n_obs), 96, 0, s>>>(
-        sp, ep, reinterpret_cast<const int4*>(lists), counts, n_obs, tiles_x, T);
+    {
+        KScope ks(s, "pull_tables", entries * (sizeof(tile::TabA) + 16.0));
+        pull_tables_kernel<<<dim3(n_tiles, n_obs), 96, 0, s>>>(
+            sp, ep, reinterpret_cast<const int4*>(lists), counts, n_obs, tiles_x, T);
+    }
+    // the touched tiles' state read and written once (24 B/cell), every (member, obs)
+    // window once, the tables once
+    KScope ks(s, "pull_apply", (24.0 * touched_cells + 8.0 * WIN * WIN * n_obs) * M +
+                                   entries * sizeof(tile::TabA));
     pull_apply_kernel<<<dim3(n_tiles, M), tile::NT, 0, s>>>(sp, ep, win, n_obs,
                                                        reinterpret_cast<const int4*>(lists), counts,
                                                        tiles_x, T, eta, hu, hv, err, err_pos);
@@ -683,16 +695,20 @@ void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
 void launch_perp_pair(cudaStream_t s, const ErrParams& ep, uint64_t seed, int64_t member_base,
                       uint64_t cycle, double ratio, double* xi, double* nu, int* foffs,
                       double* scal, const int* err, int M) {
+    // xi, nu~ written, read back for the dot products, nu written again
+    KScope ks(s, "perp_pair", 40.0 * ep.nxc * ep.nyc * M);
     perp_pair_kernel<<<M, 256, 0, s>>>(ep, seed, member_base, cycle, ratio, xi, nu, foffs, scal,
                                        err);
 }
 
 void launch_gather_cz(cudaStream_t s, int M, const double* scal, double* cz) {
+    KScope ks(s, "gather_cz", 32.0 * M);
     gather_cz_kernel<<<(M + 127) / 128, 128, 0, s>>>(M, scal, cz);
 }
 
 void launch_barrier_alpha(cudaStream_t s, const double* cz_all, int n_total, int M, double n_psi,
                           int one_stage, double* scal, double* wb, int* err) {
+    KScope ks(s, "barrier_alpha", 16.0 * n_total + 40.0 * M);
     barrier_alpha_kernel<<<1, 256, 0, s>>>(cz_all, n_total, M, n_psi, scal, wb, err, one_stage);
 }
 
@@ -705,6 +721,7 @@ void launch_local_blocks(cudaStream_t s, const ErrParams& ep, const double* xi, 
     const size_t full = (49 * 49 + nr) * sizeof(double);
     const int in_smem = full <= 160 * 1024;
     smem_opt_in(local_blocks_kernel, 160 * 1024);
+    KScope ks(s, "local_blocks", 24.0 * nr * M);  // xi, nu read, z written
     local_blocks_kernel<<<M, 64 * kLbGroups, in_smem ? full : 49 * 49 * sizeof(double), s>>>(
         ep, xi, nu, scal, wb, cells, n_obs, order, level_start, n_levels, foffs, usig, z, err,
         in_smem, one_stage);
@@ -714,12 +731,15 @@ void launch_drifters(cudaStream_t s, const SweParams& sp, const float* eta, cons
                      const float* hv, int M, int n_d, double dt, double* pos, int* wind, int* err,
                      int* err_pos) {
     const int n = M * n_d;
+    // per drifter: 12 B state gather, position and winding counts read and written
+    KScope ks(s, "drifters", 60.0 * n);
     drifters_kernel<<<(n + 127) / 128, 128, 0, s>>>(sp, eta, hu, hv, M, n_d, dt, pos, wind, err,
                                                     err_pos);
 }
 
 void launch_observe_mooring(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
                             const float* hv, int m, const double* xy, int n, double* y, int* bad) {
+    KScope ks(s, "observe_mooring", 44.0 * n);
     observe_mooring_kernel<<<(n + 127) / 128, 128, 0, s>>>(sp, eta, hu, hv, m, xy, n, y, bad);
 }
 

@@ -31,6 +31,8 @@ struct IewpfBuffers {
     int n_total = 0;
     uint64_t cycle = 0;
     int one_stage = 0;        // dc_iewpf_set_mode
+    bool pending = false;     // dc_iewpf_begin done, dc_iewpf_finish not yet: the obs /
+                              // cells / S d buffers belong to that analysis
     double S_host[4] = {0, 0, 0, 0};
     std::vector<double> usig_host;
     bool usig_valid = false;
@@ -46,7 +48,11 @@ struct IewpfBuffers {
     int* lb_start = nullptr;  // [cap_obs + 1] first position of each level in lb_order
     int lb_levels = 0;
     std::vector<double> lb_xy;  // observation positions the schedule was built for
-    std::vector<int> lb_host;   // host copy of order + start (source of the async upload)
+    std::vector<int> lb_host;   // host copy of order + start, uploaded from the pinned
+    bool lb_dirty = false;      // staging slot of the next upload_obs when dirty
+    // pull footprint of the current observation set (algorithmic bytes of the pull, kprof):
+    // (tile, covering obs) entries and the cells of the tiles at least one obs touches
+    double pull_entries = 0.0, pull_cells = 0.0;
     // drifters
     int n_d = 0;
     double* dpos = nullptr;   // [M][n_d][2]

@@ -23,7 +23,7 @@ size_t pull_table_bytes();
 void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep, const double* win,
                        const int* cells, int n_obs, const int* lists, const int* counts,
                        int n_tiles, int tiles_x, void* tabs, float* eta, float* hu, float* hv,
-                       int* err, int* err_pos, int M);
+                       int* err, int* err_pos, int M, double entries, double touched_cells);
 void launch_perp_pair(cudaStream_t s, const ErrParams& ep, uint64_t seed, int64_t member_base,
                       uint64_t cycle, double ratio, double* xi, double* nu, int* foffs,
                       double* scal, const int* err, int M);

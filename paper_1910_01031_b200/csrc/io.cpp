@@ -117,6 +117,14 @@ std::string particle_path(const std::string& dir, int64_t id) {
     return dir + "/ensemble/particle_" + std::to_string(id) + ".dcst";
 }
 
+std::string drifters_path(const std::string& dir, int64_t id) {
+    return dir + "/ensemble/particle_" + std::to_string(id) + ".drifters";
+}
+
+std::string rng_path(const std::string& dir, int64_t first) {
+    return dir + "/rng_state_" + std::to_string(first) + ".txt";
+}
+
 std::string fmt17(double v) {
     char b[40];
     std::snprintf(b, sizeof(b), "%.17g", v);
@@ -181,14 +189,38 @@ dc_status dc_checkpoint_save(dc_ctx* ctx, const char* dir, uint64_t filter_cycle
         st = write_snapshot(ctx, particle_path(d, base + m), cfg.nx, cfg.ny, s);
         if (st) return st;
     }
-    uint64_t draw = 0;
+    // drifter copies with their winding counts (dc_da_cycle advects them: a resume
+    // without them would not be bitwise)
+    int32_t n_d = 0;
+    if (dc_drifters_count(ctx, &n_d) == DC_OK && n_d > 0) {
+        std::vector<double> pos(static_cast<size_t>(M) * n_d * 2);
+        std::vector<int32_t> wind(pos.size());
+        st = dc_drifters_get(ctx, pos.data(), wind.data());
+        if (st) return st;
+        for (int m = 0; m < M; ++m) {
+            std::ofstream os(drifters_path(d, base + m));
+            for (int q = 0; q < n_d; ++q) {
+                const size_t i = (static_cast<size_t>(m) * n_d + q) * 2;
+                os << q << "," << fmt17(pos[i]) << "," << fmt17(pos[i + 1]) << "," << wind[i]
+                   << "," << wind[i + 1] << "\n";
+            }
+            if (!os) return dcg::ctx_error(ctx, DC_EIO, "checkpoint: cannot write drifters", -1);
+        }
+    }
+    uint64_t draw = 0, tag = 1;
+    int32_t mode = 0;
     dc_get_draw_counter(ctx, &draw);
+    dc_get_model_error_tag(ctx, &tag);
+    dc_iewpf_get_mode(ctx, &mode);
     {
-        std::ofstream os(d + "/rng_state.txt");
+        std::ofstream os(rng_path(d, base));
         os << "seed " << cfg.seed << "\n"
            << "model_error_draw " << draw << "\n"
-           << "filter_cycle " << filter_cycle << "\n";
-        if (!os) return dcg::ctx_error(ctx, DC_EIO, "checkpoint: cannot write rng_state.txt", -1);
+           << "model_error_tag " << tag << "\n"
+           << "filter_cycle " << filter_cycle << "\n"
+           << "iewpf_mode " << mode << "\n"
+           << "drifters " << n_d << "\n";
+        if (!os) return dcg::ctx_error(ctx, DC_EIO, "checkpoint: cannot write rng_state", -1);
     }
     {
         std::ofstream os(d + "/meta.txt");
@@ -319,10 +351,11 @@ dc_status dc_checkpoint_load(dc_ctx* ctx, const char* dir, uint64_t* filter_cycl
     int32_t M = 0;
     int64_t base = 0;
     dc_get_config(ctx, &cfg, &M, &base);
-    uint64_t seed = 0, draw = 0, cycle = 0;
+    uint64_t seed = 0, draw = 0, cycle = 0, tag = 1, mode = 0, n_d = 0;
     {
-        std::ifstream is(d + "/rng_state.txt");
-        if (!is) return dcg::ctx_error(ctx, DC_EIO, "checkpoint: cannot open rng_state.txt", -1);
+        std::ifstream is(rng_path(d, base));
+        if (!is) is.open(d + "/rng_state.txt");
+        if (!is) return dcg::ctx_error(ctx, DC_EIO, "checkpoint: cannot open rng_state", -1);
         std::string key;
         uint64_t val = 0;
         int seen = 0;
@@ -330,8 +363,11 @@ dc_status dc_checkpoint_load(dc_ctx* ctx, const char* dir, uint64_t* filter_cycl
             if (key == "seed") seed = val, seen |= 1;
             else if (key == "model_error_draw") draw = val, seen |= 2;
             else if (key == "filter_cycle") cycle = val, seen |= 4;
+            else if (key == "model_error_tag") tag = val;
+            else if (key == "iewpf_mode") mode = val;
+            else if (key == "drifters") n_d = val;
         }
-        if (seen != 7) return dcg::ctx_error(ctx, DC_EIO, "checkpoint: malformed rng_state.txt", -1);
+        if (seen != 7) return dcg::ctx_error(ctx, DC_EIO, "checkpoint: malformed rng_state", -1);
     }
     if (seed != cfg.seed)
         return dcg::ctx_error(ctx, DC_EINVAL,
@@ -345,7 +381,36 @@ dc_status dc_checkpoint_load(dc_ctx* ctx, const char* dir, uint64_t* filter_cycl
         st = dc_upload_member(ctx, m, s.eta.data(), s.hu.data(), s.hv.data(), s.t);
         if (st) return st;
     }
+    if (n_d > 0) {
+        std::vector<double> pos(static_cast<size_t>(M) * n_d * 2);
+        std::vector<int32_t> wind(pos.size());
+        for (int m = 0; m < M; ++m) {
+            std::ifstream is(drifters_path(d, base + m));
+            if (!is) return dcg::ctx_error(ctx, DC_EIO, "checkpoint: cannot open drifters", m);
+            std::string line;
+            for (uint64_t q = 0; q < n_d; ++q) {
+                if (!std::getline(is, line))
+                    return dcg::ctx_error(ctx, DC_EIO, "checkpoint: truncated drifters file", m);
+                unsigned long long id = 0;
+                long long wx = 0, wy = 0;
+                double x = 0.0, y = 0.0;
+                if (std::sscanf(line.c_str(), "%llu,%lf,%lf,%lld,%lld", &id, &x, &y, &wx, &wy) != 5 ||
+                    id != q)
+                    return dcg::ctx_error(ctx, DC_EIO, "checkpoint: malformed drifters file", m);
+                const size_t i = (static_cast<size_t>(m) * n_d + q) * 2;
+                pos[i] = x;
+                pos[i + 1] = y;
+                wind[i] = static_cast<int32_t>(wx);
+                wind[i + 1] = static_cast<int32_t>(wy);
+            }
+        }
+        dc_status st = dc_drifters_restore(ctx, pos.data(), wind.data(), static_cast<int32_t>(n_d));
+        if (st) return st;
+    }
     dc_set_draw_counter(ctx, draw);
+    dc_status st = dc_set_model_error_tag(ctx, tag);
+    if (st) return st;
+    if ((st = dc_iewpf_set_mode(ctx, static_cast<int32_t>(mode)))) return st;
     if (filter_cycle) *filter_cycle = cycle;
     return DC_OK;
 }

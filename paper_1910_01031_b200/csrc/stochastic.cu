@@ -264,6 +264,7 @@ void launch_philox_noise(cudaStream_t s, const ErrParams& ep, int M, uint64_t se
                          int* offsets, const int* err) {
     const int npairs = (ep.nxc * ep.nyc + 1) / 2;
     int bx = (npairs + 255) / 256;
+    KScope ks(s, "philox_noise", 8.0 * ep.nxc * ep.nyc * M);
     philox_noise_kernel<<<dim3(bx, M), 256, 0, s>>>(ep, M, seed, tag, member_base, substream,
                                                     draw, xi, offsets, err);
 }
@@ -273,6 +274,7 @@ void launch_philox_soar(cudaStream_t s, const ErrParams& ep, int M, uint64_t see
                         int* offsets, const int* err) {
     const size_t bytes = static_cast<size_t>(kBand + 4) * ep.nxc * sizeof(double);
     smem_opt_in(philox_soar_kernel, 200 * 1024);
+    KScope ks(s, "philox_soar", 8.0 * ep.nxc * ep.nyc * M);  // xi stays on chip
     philox_soar_kernel<<<dim3((ep.nyc + kBand - 1) / kBand, M), 256, bytes, s>>>(
         ep, M, seed, tag, member_base, substream, draw, corr, offsets, err);
 }
@@ -280,13 +282,18 @@ void launch_philox_soar(cudaStream_t s, const ErrParams& ep, int M, uint64_t see
 void launch_coarse_soar(cudaStream_t s, const ErrParams& ep, int M, const double* in,
                         double* out, const int* err) {
     const int nr = ep.nxc * ep.nyc;
+    KScope ks(s, "coarse_soar", 16.0 * nr * M);
     coarse_soar_kernel<<<dim3((nr + 255) / 256, M), 256, 0, s>>>(ep, M, in, out, err);
 }
 
 void launch_q_half_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
                          const double* corr, const int* offsets, double scale, float* eta,
-                         float* hu, float* hv, int* err, int* err_pos, int M, unsigned* mx) {
+                         float* hu, float* hv, int* err, int* err_pos, int M, unsigned* mx,
+                         const char* prof_name) {
     dim3 grid((sp.nx + TX - 1) / TX, (sp.ny + TY - 1) / TY, M);
+    // the state read and written once (24 B/cell) + the coarse field
+    KScope ks(s, prof_name,
+              (24.0 * sp.nx * sp.ny + 8.0 * ep.nxc * ep.nyc) * M);
     q_half_apply_kernel<<<grid, tile::NT, 0, s>>>(sp, ep, corr, offsets, scale, eta, hu, hv, err,
                                              err_pos, mx);
 }

@@ -126,6 +126,36 @@ class Ensemble:
         self._ck(self.L.dc_time_stages(self.h, n_substeps, _d(out)))
         return float(out[0]), float(out[1])
 
+    # ---- multi-GPU (dc_comm_*: NCCL inside the library) ----
+    def comm_attach(self, nccl_id: bytes, rank: int, world: int, n_total: int):
+        """Join the ranks' NCCL communicator (collective). nccl_id: the 128 bytes of
+        comm_unique_id() made on rank 0 and broadcast by the host driver."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(nccl_id))
+        self._ck(self.L.dc_comm_attach(self.h, buf, rank, world, n_total))
+
+    def comm_detach(self):
+        self._ck(self.L.dc_comm_detach(self.h))
+
+    def comm_info(self):
+        r, w, n = C.c_int32(), C.c_int32(), C.c_int64()
+        self._ck(self.L.dc_comm_info(self.h, C.byref(r), C.byref(w), C.byref(n)))
+        return r.value, w.value, n.value
+
+    def profile_begin(self):
+        """Open a per-kernel profile window (dc_profile_begin): every kernel launched by
+        this thread until profile_end is timed with CUDA events on its stream."""
+        self._ck(self.L.dc_profile_begin(self.h))
+
+    def profile_end(self):
+        """Close the window: [(kernel, launches, total ms, total algorithmic bytes)] in
+        first-launch order."""
+        cap = 64
+        out = (_lib.DcKernelTime * cap)()
+        n = C.c_int32()
+        self._ck(self.L.dc_profile_end(self.h, out, cap, C.byref(n)))
+        return [(out[i].name.decode(), int(out[i].launches), float(out[i].ms), float(out[i].bytes))
+                for i in range(min(n.value, cap))]
+
     # ---- state I/O ----
     def upload(self, eta, hu, hv, t=None):
         eta, hu, hv = (np.ascontiguousarray(a, np.float32) for a in (eta, hu, hv))
@@ -227,8 +257,14 @@ class Ensemble:
         pos = np.ascontiguousarray(pos, np.float64)
         if pos.ndim == 2:
             pos = np.ascontiguousarray(np.broadcast_to(pos, (self.n,) + pos.shape))
-        self.n_drifters = pos.shape[1]
         self._ck(self.L.dc_drifters_set(self.h, _d(pos), pos.shape[1]))
+
+    @property
+    def n_drifters(self) -> int:
+        """drifter copies per member (set by drifters_set or a checkpoint load)."""
+        n = C.c_int32()
+        rc = self.L.dc_drifters_count(self.h, C.byref(n))
+        return n.value if rc == 0 else 0
 
     def advect_drifters(self, dt):
         self._ck(self.L.dc_drifters_advect(self.h, dt))
@@ -394,6 +430,16 @@ class Ensemble:
         S = np.ascontiguousarray(S, np.float64).reshape(4)
         usig = np.ascontiguousarray(usig, np.float64).reshape(49 * 49)
         self._ck(self.L.dc_da_cycle(self.h, n_steps, arr, n, _d(S), _d(usig), cycle))
+
+
+def comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for dc_comm_attach; made on rank 0."""
+    L = _lib.load()
+    buf = (C.c_uint8 * 128)()
+    rc = L.dc_comm_unique_id(buf)
+    if rc:
+        raise DcError(rc, "dc_comm_unique_id failed (NCCL not loadable?)")
+    return bytes(buf)
 
 
 def forecast_error_gathered(cfg: Config, n_members, n_drifters, pos_ptr, wind_ptr, truth_xy,

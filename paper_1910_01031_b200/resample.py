@@ -44,9 +44,13 @@ def exchange_plan(idx, per_rank: int, rank: int):
     return local_idx, sorted(sends), recvs
 
 
-def exchange(plan, nbytes, new_buffer, export_fn, gather_fn, import_fn, dist, sync_fn=None):
+def exchange(plan, nbytes, new_buffer, export_fn, gather_fn, import_fn, dist, sync_fn=None,
+             transport_done=None):
     """Run a plan: export the sent members (before the local gather overwrites them),
-    exchange over dist point-to-point, gather locally, import the received members."""
+    exchange over dist point-to-point, gather locally, import the received members.
+    transport_done() must block until the received buffers hold their data: with NCCL,
+    req.wait() only orders torch's current stream after the transfer, while the imports
+    run on the Ensemble's own stream."""
     local_idx, sends, recvs = plan
     sbufs = []
     for dest, src in sends:
@@ -61,6 +65,8 @@ def exchange(plan, nbytes, new_buffer, export_fn, gather_fn, import_fn, dist, sy
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+        if transport_done:
+            transport_done()
     gather_fn(local_idx)
     for (_, _, slots), (_, b) in zip(recvs, rbufs):
         for i in slots:
@@ -80,4 +86,6 @@ def resample_across_ranks(ens, idx, dist, device):
              lambda m, b: ens.member_export(m, b.data_ptr()),
              lambda li: ens.resample_members(li),
              lambda m, b: ens.member_import(m, b.data_ptr()),
-             dist, sync_fn=ens.sync)
+             dist, sync_fn=ens.sync,
+             transport_done=(lambda: torch.cuda.current_stream(device).synchronize())
+             if str(device).startswith("cuda") else None)

@@ -219,14 +219,17 @@ def test_checkpoint_resume_is_bitwise(oracle, tmp_path):
                       rng.normal(0, 20.0, (6, 2))]) for _ in range(4)]
     _, S = pkg.precompute_S(cfg)
     _, usig = pkg.precompute_local_svd(cfg, S)
+    pos = np.random.default_rng(7).uniform(0, 1, size=(n, 5, 2)) * [p.nx * p.dx, p.ny * p.dy]
     a = pkg.Ensemble(cfg, n)
     a.upload(e, u, v, 0.0)
+    a.drifters_set(pos)  # drifter copies are advected by every cycle: they must resume too
     for c in range(2):
         a.da_cycle(5, obs[c], S, usig, c)
     a.checkpoint_save(tmp_path / "ck", filter_cycle=2)
     for c in range(2, 4):
         a.da_cycle(5, obs[c], S, usig, c)
     want = a.download()
+    want_d = a.drifters_get()
     b = pkg.Ensemble(cfg, n)
     cyc = b.checkpoint_load(tmp_path / "ck")
     assert cyc == 2 and b.draw_counter == a.draw_counter - 8
@@ -235,8 +238,11 @@ def test_checkpoint_resume_is_bitwise(oracle, tmp_path):
     got = b.download()
     for x, y in zip(want, got):
         assert np.array_equal(x, y)
+    got_d = b.drifters_get()
+    assert np.array_equal(want_d[0], got_d[0]) and np.array_equal(want_d[1], got_d[1])
     names = sorted(os.listdir(tmp_path / "ck" / "ensemble"))
-    assert names == [f"particle_{i}.dcst" for i in range(n)]
+    assert names == sorted([f"particle_{i}.dcst" for i in range(n)] +
+                           [f"particle_{i}.drifters" for i in range(n)])
 
 
 def test_trajectory_file(tmp_path):

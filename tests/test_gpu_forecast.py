@@ -135,18 +135,41 @@ def test_model_step_bitwise_shapes(oracle, nx, ny, n):
     _step_vs_oracle(oracle, nx, ny, n, 2, seed=nx + ny)
 
 
-# launch-shape knobs read at context creation: strip heights, tail strips, the separate
-# substep_end launch, the host-driven substep loop, the persistent one-launch step (with
-# several strip heights) -- all must give the same bits
-@pytest.mark.parametrize("env", [{"DC_TAIL_ROWS": "0"}, {"DC_TAIL_ROWS": "7", "DC_TAIL_STRIPS": "3"},
-                                 {"DC_STRIP_ROWS": "13"}, {"DC_FUSED_END": "0"},
-                                 {"DC_NO_GRAPH": "1"}, {"DC_NO_GRAPH": "1", "DC_FUSED_END": "0"},
-                                 {"DC_PERSISTENT": "1"},
-                                 {"DC_PERSISTENT": "1", "DC_PSTRIP_ROWS": "7"}])
+# the two substep-loop paths: the graph while-node (default) and the host-driven loop
+# (DC_NO_GRAPH=1, also what a dc_profile window uses) -- both must give the same bits
+@pytest.mark.parametrize("env", [{}, {"DC_NO_GRAPH": "1"}])
 def test_model_step_bitwise_launch_variants(oracle, monkeypatch, env):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _step_vs_oracle(oracle, 500, 300, 3, 2, seed=11)
+
+
+def test_profile_window_is_bitwise_and_complete(oracle):
+    """dc_profile_begin/end: the stage kernels run one by one inside the window (host
+    loop), results stay bitwise, and every launch is reported with its algorithmic bytes
+    (24 / 36 B per cell for the two stages)."""
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair(500, 300)
+    e, u, v = perturbed_jets(oracle, p, 3, seed=12)
+    ens = Ensemble(cfg, 3)
+    ens.upload(e, u, v, 0.0)
+    ens.profile_begin()
+    ens.model_step(2)
+    prof = {name: (n, ms, b) for name, n, ms, b in ens.profile_end()}
+    ge, gu, gv, gt = ens.download()
+    subs = 0
+    for m in range(3):
+        s = State(e[m].copy(), u[m].copy(), v[m].copy(), 0.0)
+        dts = oracle.model_step(p, s, 2)
+        subs = max(subs, len(dts))
+        assert np.array_equal(ge[m], s.eta) and np.array_equal(gu[m], s.hu)
+        assert np.array_equal(gv[m], s.hv)
+    n1, ms1, b1 = prof["swe_stage_pair<1>"]
+    n2, ms2, b2 = prof["swe_stage_pair<2>"]
+    assert n1 == n2 >= subs and ms1 > 0 and ms2 > 0
+    assert b1 == n1 * 24.0 * 3 * 500 * 300 and b2 == n2 * 36.0 * 3 * 500 * 300
+    assert prof["step_begin"][0] == 2 and "fix_ghosts" in prof
+    ens.close()
 
 
 def test_model_step_fma_tolerance(oracle):
@@ -327,9 +350,7 @@ def test_non_finite_state_reported_like_reference(oracle, ref, field, value):
 # every substep-loop variant must retire errored members and finish the step: a member
 # dry at step start (never steps), one poisoned mid-substep (non-finite), all members dry
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("env", [{}, {"DC_FUSED_END": "0"}, {"DC_NO_GRAPH": "1"},
-                                 {"DC_NO_GRAPH": "1", "DC_FUSED_END": "0"},
-                                 {"DC_PERSISTENT": "1"}])
+@pytest.mark.parametrize("env", [{}, {"DC_NO_GRAPH": "1"}])
 def test_errored_members_retire_in_every_loop_variant(oracle, monkeypatch, env):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -359,4 +380,37 @@ def test_errored_members_retire_in_every_loop_variant(oracle, monkeypatch, env):
     with pytest.raises(DcError):
         ens.model_step(1)
         ens.sync()
+    ens.close()
+
+
+def test_failed_member_recovers_when_overwritten(oracle):
+    """A member that failed (dry cell) is healthy again once its state is overwritten --
+    re-uploaded, or resampled from a healthy particle -- and then steps bitwise like the
+    oracle (the reference throws per call and never poisons a particle)."""
+    _, Ensemble = _gpu()
+    from paper_1910_01031_b200 import DcError
+    cfg, p = cfg_pair(100, 60)
+    e, u, v = perturbed_jets(oracle, p, 3, seed=8)
+    bad = e.copy()
+    bad[1, 10, 20] = -231.0
+    ens = Ensemble(cfg, 3)
+    ens.upload(bad, u, v, 0.0)
+    with pytest.raises(DcError):
+        ens.model_step(1)
+        ens.sync()
+    ens.upload_member(1, e[1], u[1], v[1], 0.0)  # reload the failed particle
+    ens.model_step(1)  # every member steps now (no error surfaces)
+    ge, gu, gv, gt = ens.download()
+    s = State(e[1].copy(), u[1].copy(), v[1].copy(), 0.0)
+    oracle.model_step(p, s, 1)
+    assert np.array_equal(ge[1], s.eta) and np.array_equal(gu[1], s.hu) and gt[1] == 60.0
+    # resampling a failed slot from a healthy source clears it; a failed source carries its
+    # error into the slots that copy it
+    ens.upload(bad, u, v, 0.0)
+    with pytest.raises(DcError):
+        ens.model_step(1)
+        ens.sync()
+    ens.resample_members(np.array([0, 0, 2], np.int32))
+    ens.model_step(1)
+    ens.sync()
     ens.close()

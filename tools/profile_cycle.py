@@ -1,5 +1,5 @@
 """Profiling driver: one warm-up + one measured IEWPF cycle of the bench workload
-(100 members, 500x300, 64 drifters or 240 moorings) with synthetic observations made on
+(--members, --nx x --ny, 64 drifters or 240 moorings) with synthetic observations made on
 the host, so every kernel launch belongs to the ensemble (no truth run). Use with
 DC_NO_GRAPH=1 so ncu sees the stage kernels as individual launches."""
 import argparse
@@ -16,10 +16,13 @@ def main():
     ap.add_argument("--obs", default="drifters", choices=["drifters", "moorings"])
     ap.add_argument("--members", type=int, default=100)
     ap.add_argument("--cycles", type=int, default=2)
+    ap.add_argument("--nx", type=int, default=500)
+    ap.add_argument("--ny", type=int, default=300)
     a = ap.parse_args()
     import paper_1910_01031_b200 as pkg
     from bench import platforms
-    cfg = pkg.Config()
+    dx = 2220.0 * 500 / a.nx
+    cfg = pkg.Config(nx=a.nx, ny=a.ny, dx=dx, dy=dx)
     ens = pkg.Ensemble(cfg, a.members)
     ens.init_double_jet()
     pos = platforms(cfg, a.obs)
