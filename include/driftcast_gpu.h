@@ -365,6 +365,13 @@ dc_status dc_profile_begin(dc_ctx* ctx);
 dc_status dc_profile_end(dc_ctx* ctx, dc_kernel_time* out, int32_t cap, int32_t* n_out);
 /* the cudaStream_t the context runs on. */
 void* dc_stream(dc_ctx* ctx);
+/* Memory checker (no compute-sanitizer on the GPU pool): with DC_GUARD=1 in the
+ * environment every device buffer of the library is allocated with 64 KB guard bands
+ * (byte pattern) on both sides and its contents poisoned (0xFF bytes: NaN floats) before
+ * first use. Synchronises the device and verifies every live guard band: DC_ECUDA and a
+ * description (allocation site, side, offset) when a kernel wrote out of bounds; DC_OK
+ * (n_bad = 0) otherwise or without DC_GUARD. */
+dc_status dc_check_guards(char* msg, int32_t cap, int32_t* n_bad);
 /* Exhaustive device self-check of the branch-free IEEE sqrt / reciprocal used by the
  * stencil against the CUDA intrinsics over all positive normal floats (synchronous).
  * counts[0..1] = sqrt / rcp mismatches, counts[2..3] = first mismatching operand bits. */

@@ -89,7 +89,7 @@ EXPORTS = [
     "dc_readback_enqueue", "dc_readback_wait", "dc_member_bytes", "dc_member_export",
     "dc_member_import", "dc_profile_begin", "dc_profile_end", "dc_comm_unique_id",
     "dc_comm_attach", "dc_comm_detach", "dc_comm_info", "dc_drifters_restore",
-    "dc_get_model_error_tag", "dc_iewpf_get_mode",
+    "dc_get_model_error_tag", "dc_iewpf_get_mode", "dc_check_guards",
 ]
 
 
@@ -161,6 +161,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "dc_drifters_restore": (st, [vp, dp, ip, C.c_int32]),
         "dc_get_model_error_tag": (st, [vp, C.POINTER(C.c_uint64)]),
         "dc_iewpf_get_mode": (st, [vp, ip]),
+        "dc_check_guards": (st, [C.c_char_p, C.c_int32, ip]),
         "dc_comm_info": (st, [vp, ip, ip, C.POINTER(C.c_int64)]),
         "dc_profile_end": (st, [vp, C.POINTER(DcKernelTime), C.c_int32, ip]),
         "dc_drifters_count": (st, [vp, ip]),

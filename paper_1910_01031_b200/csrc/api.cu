@@ -522,7 +522,7 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
         const int n_tail = ctx->sp.ny >= 4 * ctx->sp.by ? 2 : 0;
         if (tail_rows > 0 && n_tail > 0 && tail_rows * n_tail < ctx->sp.ny && ctx->sp.ny < 32768) {
             const std::vector<int2> u = build_units(ctx->sp, tail_rows, n_tail);
-            CU(cudaMalloc(&ctx->units, u.size() * sizeof(int2)));
+            CU(DMALLOC(&ctx->units, u.size() * sizeof(int2)));
             CU(cudaMemcpy(ctx->units, u.data(), u.size() * sizeof(int2), cudaMemcpyHostToDevice));
             ctx->sp.units = ctx->units;
             ctx->sp.n_units = static_cast<int>(u.size());
@@ -541,7 +541,7 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     const size_t origin = 2 * static_cast<size_t>(ctx->sp.pitch) + 2;
     for (int s = 0; s < 2; ++s) {
         const size_t bytes = 3 * ctx->field_elems * sizeof(float);
-        CU(cudaMalloc(&ctx->blk[s], bytes));
+        CU(DMALLOC(&ctx->blk[s], bytes));
         CU(cudaMemsetAsync(ctx->blk[s], 0, bytes, ctx->stream));
         for (int i = 0; i < 3; ++i) ctx->f[3 * s + i] = ctx->blk[s] + i * ctx->field_elems + origin;
         if (!make_state_map(&ctx->maps[s], ctx->blk[s], ctx->sp, ctx->field_elems))
@@ -550,7 +550,7 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     const int M = ctx->M;
     // 17 arrays, each rounded up to 16 bytes by take()
     size_t bytes = 17 * ((static_cast<size_t>(M) * 4 * sizeof(double) + 15) / 16 * 16) + 64;
-    CU(cudaMalloc(&ctx->ctl_mem, bytes));
+    CU(DMALLOC(&ctx->ctl_mem, bytes));
     CU(cudaMemsetAsync(ctx->ctl_mem, 0, bytes, ctx->stream));
     char* p = static_cast<char*>(ctx->ctl_mem);
     auto take = [&](size_t n) {
@@ -571,8 +571,8 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     ctx->ctl.any_active = reinterpret_cast<int*>(take(sizeof(int)));
     ctx->ctl.n_active = reinterpret_cast<int*>(take(sizeof(int)));
     ctx->ctl.mdone = reinterpret_cast<unsigned*>(take(M * sizeof(unsigned)));
-    CU(cudaMalloc(&ctx->substep_iters, 2 * sizeof(unsigned long long)));
-    CU(cudaMalloc(&ctx->host_iters, 2 * sizeof(unsigned long long)));
+    CU(DMALLOC(&ctx->substep_iters, 2 * sizeof(unsigned long long)));
+    CU(DMALLOC(&ctx->host_iters, 2 * sizeof(unsigned long long)));
     CU(cudaMemsetAsync(ctx->host_iters, 0, 2 * sizeof(unsigned long long), ctx->stream));
     CU(cudaMemsetAsync(ctx->substep_iters, 0, 2 * sizeof(unsigned long long), ctx->stream));
     // accumulators: max fields 0, min field all-ones (ordered +inf side), err_pos INT_MAX
@@ -588,11 +588,11 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     std::vector<int> big(M, 0x7fffffff);
     CU(cudaMemcpyAsync(ctx->ctl.err_pos, big.data(), M * sizeof(int), cudaMemcpyHostToDevice,
                        ctx->stream));
-    CU(cudaMalloc(&ctx->xi, static_cast<size_t>(M) * ctx->nr * sizeof(double)));
-    CU(cudaMalloc(&ctx->corr, static_cast<size_t>(M) * ctx->nr * sizeof(double)));
-    CU(cudaMalloc(&ctx->offs, 2 * M * sizeof(int)));
+    CU(DMALLOC(&ctx->xi, static_cast<size_t>(M) * ctx->nr * sizeof(double)));
+    CU(DMALLOC(&ctx->corr, static_cast<size_t>(M) * ctx->nr * sizeof(double)));
+    CU(DMALLOC(&ctx->offs, 2 * M * sizeof(int)));
     CU(cudaMemsetAsync(ctx->offs, 0, 2 * M * sizeof(int), ctx->stream));
-    CU(cudaMalloc(&ctx->gmax, 2 * M * sizeof(unsigned long long)));
+    CU(DMALLOC(&ctx->gmax, 2 * M * sizeof(unsigned long long)));
     CU(cudaStreamSynchronize(ctx->stream));
     return DC_OK;
 }
@@ -603,16 +603,16 @@ dc_status dc_destroy(dc_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->step_exec) cudaGraphExecDestroy(ctx->step_exec);
     if (ctx->step_exec_fused) cudaGraphExecDestroy(ctx->step_exec_fused);
-    for (auto* q : ctx->blk) cudaFree(q);
-    cudaFree(ctx->ctl_mem);
-    if (ctx->units) cudaFree(ctx->units);
-    cudaFree(ctx->substep_iters);
-    cudaFree(ctx->host_iters);
-    cudaFree(ctx->xi);
-    cudaFree(ctx->corr);
-    cudaFree(ctx->offs);
-    cudaFree(ctx->gmax);
-    cudaFree(ctx->rhs);
+    for (auto* q : ctx->blk) dcg::dfree(q);
+    dcg::dfree(ctx->ctl_mem);
+    if (ctx->units) dcg::dfree(ctx->units);
+    dcg::dfree(ctx->substep_iters);
+    dcg::dfree(ctx->host_iters);
+    dcg::dfree(ctx->xi);
+    dcg::dfree(ctx->corr);
+    dcg::dfree(ctx->offs);
+    dcg::dfree(ctx->gmax);
+    dcg::dfree(ctx->rhs);
     iewpf_free(ctx->iw);
     fe_free(ctx->fe);
     readback_free(ctx->rb);
@@ -804,7 +804,7 @@ dc_status dc_flux_rhs(dc_ctx* ctx, int32_t m, float* d_eta, float* d_hu, float* 
     dc_status st = check_member(ctx, m);
     if (st) return st;
     const size_t per = ctx->sp.mstride;
-    if (!ctx->rhs) CU(cudaMalloc(&ctx->rhs, 3 * per * sizeof(float)));  // per = mstride
+    if (!ctx->rhs) CU(DMALLOC(&ctx->rhs, 3 * per * sizeof(float)));  // per = mstride
     // dry-cell check of load() (swe.hpp:319): flux_rhs throws before computing
     std::vector<float> e(static_cast<size_t>(ctx->sp.nx) * ctx->sp.ny);
     CU(cudaMemcpy2DAsync(e.data(), ctx->sp.nx * sizeof(float), ctx->f[0] + m * ctx->sp.mstride,
@@ -1046,14 +1046,25 @@ dc_status dc_profile_end(dc_ctx* ctx, dc_kernel_time* out, int32_t cap, int32_t*
     return surface_errors(ctx);
 }
 
+dc_status dc_check_guards(char* msg, int32_t cap, int32_t* n_bad) {
+    std::string m;
+    const int bad = check_guards(&m);
+    if (n_bad) *n_bad = bad;
+    if (msg && cap > 0) {
+        std::strncpy(msg, m.c_str(), cap - 1);
+        msg[cap - 1] = 0;
+    }
+    return bad ? DC_ECUDA : DC_OK;
+}
+
 dc_status dc_selftest_math(int32_t device, uint64_t* counts) {
     if (cudaSetDevice(device) != cudaSuccess) return DC_ECUDA;
     unsigned long long* d = nullptr;
-    if (cudaMalloc(&d, 4 * sizeof(unsigned long long)) != cudaSuccess) return DC_ECUDA;
+    if (DMALLOC(&d, 4 * sizeof(unsigned long long)) != cudaSuccess) return DC_ECUDA;
     cudaMemset(d, 0, 4 * sizeof(unsigned long long));
     launch_selftest_math(nullptr, d);
     cudaError_t e = cudaMemcpy(counts, d, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-    cudaFree(d);
+    dcg::dfree(d);
     return e == cudaSuccess ? DC_OK : DC_ECUDA;
 }
 

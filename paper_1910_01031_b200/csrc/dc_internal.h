@@ -88,6 +88,16 @@ inline void smem_opt_in(F* func, size_t bytes) {
     done.fetch_or(bit);
 }
 
+// ---- device allocations (guard.cu): plain cudaMalloc, or guard-banded with DC_GUARD=1 ----
+cudaError_t dmalloc_impl(void** p, size_t bytes, const char* file, int line);
+cudaError_t dfree(void* p);
+int check_guards(std::string* msg);
+template <class T>
+inline cudaError_t dmalloc_t(T** p, size_t bytes, const char* file, int line) {
+    return dmalloc_impl(reinterpret_cast<void**>(p), bytes, file, line);
+}
+#define DMALLOC(pp, bytes) dcg::dmalloc_t((pp), (bytes), __FILE__, __LINE__)
+
 // ---- kernel profiler (kprof.cu; dc_profile_begin / dc_profile_end) ----
 // A launcher declares `KScope ks(stream, "kernel", algorithmic_bytes);` before its launch:
 // inside an open profile window (and outside stream capture) the kernel is bracketed by

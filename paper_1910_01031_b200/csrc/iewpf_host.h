@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "dc_internal.h"
+
 namespace dcg {
 
 struct IewpfBuffers {
@@ -89,8 +91,8 @@ inline void readback_free(ReadbackSlot* r) {
 }
 
 inline void fe_free(FeScratch& f) {
-    if (f.d_truth) cudaFree(f.d_truth);
-    if (f.d_out) cudaFree(f.d_out);
+    if (f.d_truth) dcg::dfree(f.d_truth);
+    if (f.d_out) dcg::dfree(f.d_out);
     if (f.h_io) cudaFreeHost(f.h_io);
     f = FeScratch{};
 }
@@ -100,7 +102,7 @@ inline void iewpf_free(IewpfBuffers& b) {
                   b.cz, b.cz_all, b.wb, b.S, b.usig, b.foffs, b.dpos, b.dwind, b.z, b.bad,
                   b.lb_order, b.lb_start};
     for (void* p : ps)
-        if (p) cudaFree(p);
+        if (p) dcg::dfree(p);
     if (b.stage) cudaFreeHost(b.stage);
     for (cudaEvent_t e : b.stage_ev)
         if (e) cudaEventDestroy(e);

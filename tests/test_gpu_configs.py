@@ -304,3 +304,54 @@ def test_comm_world1_equals_single_context(oracle):
         assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
         assert x[2] == y[2] and x[3] == y[3]
     assert ra[3] == rb[3]
+
+
+def test_guard_banded_run_is_clean_and_bitwise():
+    """The memory checker (DC_GUARD=1, csrc/guard.cu): two DA cycles with drifters and
+    forecast statistics in a process whose every device buffer has 64 KB guard bands and
+    0xFF-poisoned contents. No guard band may change (no out-of-bounds write anywhere on
+    the path), and the results must equal an unguarded run bit for bit (no kernel reads
+    uninitialised or out-of-bounds memory into a result)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    _gpu()
+    code = r'''
+import json, sys, ctypes as C
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1910_01031_b200 as pkg
+from paper_1910_01031_b200 import _lib
+cfg = pkg.Config(nx=100, ny=60)
+_, S = pkg.precompute_S(cfg)
+_, usig = pkg.precompute_local_svd(cfg, S)
+ens = pkg.Ensemble(cfg, 3)
+ens.init_double_jet()
+pos = np.random.default_rng(1).uniform(0, 1, (3, 4, 2)) * [100 * 2220.0, 60 * 2220.0]
+ens.drifters_set(pos)
+rng = np.random.default_rng(2)
+out = []
+for c in range(2):
+    obs = np.hstack([rng.uniform(0, 1, (5, 2)) * [100 * 2220.0, 60 * 2220.0], rng.normal(0, 20, (5, 2))])
+    ens.da_cycle(5, obs, S, usig, c)
+    ens.readback_enqueue(0, truth_xy=pos[0])
+    r = ens.readback_wait(0)
+    out.append([float(r["E"]), float(r["RMSE"])] + r["diag"][:, 4].tolist())
+e, u, v, t = ens.download()
+out.append([float(np.float64(e.sum())), float(np.float64(u.sum())), float(np.float64(v.sum()))])
+msg = C.create_string_buffer(4096); n = C.c_int32()
+_lib.load().dc_check_guards(msg, 4096, C.byref(n))
+ens.close()
+print(json.dumps({"bad": n.value, "msg": msg.value.decode(), "out": out}))
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for guard in ("0", "1"):
+        env = dict(os.environ, DC_GUARD=guard)
+        r = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[guard] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["1"]["bad"] == 0, res["1"]["msg"]
+    assert res["1"]["out"] == res["0"]["out"]
