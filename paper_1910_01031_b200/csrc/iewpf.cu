@@ -343,9 +343,10 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
 __global__ void __launch_bounds__(256)
 perp_pair_kernel(ErrParams ep, uint64_t seed, long long member_base, uint64_t cycle,
                  double ratio, double* xi, double* nu, int* foffs, double* scal,
-                 const int* err) {
+                 const int* /*err*/) {
+    // state independent: computed for every member (it runs concurrently with the pull
+    // chain, whose error flags it must not depend on)
     const int m = blockIdx.x;
-    if (err[m]) return;
     const int nr = ep.nxc * ep.nyc;
     const uint64_t key = det::stream_key(seed, 2 /*filter*/, static_cast<uint64_t>(member_base + m));
     double* X = xi + static_cast<size_t>(m) * nr;
@@ -447,7 +448,7 @@ constexpr int kBarrierStage = 2048;  // particles staged in shared memory (32 KB
 // c* = (w - c) - (beta - 1) zeta. One-stage IEWPF:
 // w_target = max c, c* = w - c, no nu term (beta reported as 0).
 __global__ void barrier_alpha_kernel(const double* __restrict__ cz_all, int n_total, int M,
-                                     double n_psi, double* scal, double* wb, int* err,
+                                     double n_psi, double* scal, double* wb, int* aerr,
                                      int one_stage) {
     __shared__ double s_w, s_b;
     __shared__ int s_bad;
@@ -486,10 +487,10 @@ __global__ void barrier_alpha_kernel(const double* __restrict__ cz_all, int n_to
         wb[1] = beta;
     }
     __syncthreads();
+    // errors go to aerr (merged into err after the pull chain joined, merge_err_kernel)
     for (int m = threadIdx.x; m < M; m += blockDim.x) {
-        if (err[m]) continue;
         if (s_bad) {
-            atomicCAS(err + m, 0, E_BETA);
+            aerr[m] = E_BETA;
             continue;
         }
         const double c = scal[8 * m + 0], gamma = scal[8 * m + 2], zeta = scal[8 * m + 3];
@@ -498,7 +499,7 @@ __global__ void barrier_alpha_kernel(const double* __restrict__ cz_all, int n_to
         const double x = -((t * det::exp_det(-t)) * det::exp_det(-cstar / n_psi));
         double w;
         if (!lambert_w0(x, &w)) {
-            atomicCAS(err + m, 0, E_ALPHA);
+            aerr[m] = E_ALPHA;
             continue;
         }
         scal[8 * m + 4] = -(n_psi / gamma) * w;
@@ -526,9 +527,9 @@ local_blocks_kernel(ErrParams ep, const double* __restrict__ xi, const double* _
                     const int* __restrict__ cells, int n_obs, const int* __restrict__ order,
                     const int* __restrict__ level_start, int n_levels,
                     const int* __restrict__ foffs, const double* __restrict__ usig, double* z,
-                    const int* err, int z_in_smem, int one_stage) {
+                    const int* aerr, int z_in_smem, int one_stage) {
     const int m = blockIdx.x;
-    if (err[m]) return;
+    if (aerr[m]) return;  // no alpha for this member
     extern __shared__ double dyn[];  // [49*49] U, then [nr] z when it fits
     double* U = dyn;
     __shared__ double bin[kLbGroups][49];
@@ -707,24 +708,37 @@ void launch_gather_cz(cudaStream_t s, int M, const double* scal, double* cz) {
 }
 
 void launch_barrier_alpha(cudaStream_t s, const double* cz_all, int n_total, int M, double n_psi,
-                          int one_stage, double* scal, double* wb, int* err) {
+                          int one_stage, double* scal, double* wb, int* aerr) {
     KScope ks(s, "barrier_alpha", 16.0 * n_total + 40.0 * M);
-    barrier_alpha_kernel<<<1, 256, 0, s>>>(cz_all, n_total, M, n_psi, scal, wb, err, one_stage);
+    barrier_alpha_kernel<<<1, 256, 0, s>>>(cz_all, n_total, M, n_psi, scal, wb, aerr, one_stage);
+}
+
+namespace {
+__global__ void merge_err_kernel(int M, const int* __restrict__ aerr, int* err) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m < M && aerr[m] && !err[m]) err[m] = aerr[m];
+}
+}  // namespace
+
+void launch_merge_err(cudaStream_t s, int M, const int* aerr, int* err) {
+    KScope ks(s, "merge_err", 12.0 * M);
+    merge_err_kernel<<<(M + 127) / 128, 128, 0, s>>>(M, aerr, err);
 }
 
 void launch_local_blocks(cudaStream_t s, const ErrParams& ep, const double* xi, const double* nu,
                          const double* scal, const double* wb, const int* cells, int n_obs,
                          const int* order, const int* level_start, int n_levels,
-                         const int* foffs, const double* usig, double* z, const int* err, int M,
-                         int one_stage) {
+                         const int* foffs, const double* usig, double* z, const int* err,
+                         const int* aerr, int M, int one_stage) {
     const size_t nr = static_cast<size_t>(ep.nxc) * ep.nyc;
     const size_t full = (49 * 49 + nr) * sizeof(double);
     const int in_smem = full <= 160 * 1024;
     smem_opt_in(local_blocks_kernel, 160 * 1024);
     KScope ks(s, "local_blocks", 24.0 * nr * M);  // xi, nu read, z written
     local_blocks_kernel<<<M, 64 * kLbGroups, in_smem ? full : 49 * 49 * sizeof(double), s>>>(
-        ep, xi, nu, scal, wb, cells, n_obs, order, level_start, n_levels, foffs, usig, z, err,
+        ep, xi, nu, scal, wb, cells, n_obs, order, level_start, n_levels, foffs, usig, z, aerr,
         in_smem, one_stage);
+    (void)err;
 }
 
 void launch_drifters(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,

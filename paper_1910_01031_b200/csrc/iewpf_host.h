@@ -59,6 +59,14 @@ struct IewpfBuffers {
     int n_d = 0;
     double* dpos = nullptr;   // [M][n_d][2]
     int* dwind = nullptr;     // [M][n_d][2]
+    // the pull chain (pull_windows -> tile_lists -> pull_tables -> pull_apply) runs on a
+    // second stream, concurrently with perp_pair, the barrier exchange, barrier_alpha,
+    // local_blocks and coarse_soar, which never touch the state; the posterior waits for it
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool join_pending = false;
+    int* aerr = nullptr;      // [M] barrier / alpha errors, merged into err after the join
+                              // (so a pull error keeps its precedence, as in the reference)
 };
 
 // persistent scratch of forecast_error (per-drifter E_d, RMSE_d): device truth and results,
@@ -100,9 +108,15 @@ inline void fe_free(FeScratch& f) {
 inline void iewpf_free(IewpfBuffers& b) {
     void* ps[] = {b.obs, b.cells, b.d, b.sd, b.win, b.tile_lists, b.tile_count, b.tabs, b.nu, b.scal,
                   b.cz, b.cz_all, b.wb, b.S, b.usig, b.foffs, b.dpos, b.dwind, b.z, b.bad,
-                  b.lb_order, b.lb_start};
+                  b.lb_order, b.lb_start, b.aerr};
     for (void* p : ps)
         if (p) dcg::dfree(p);
+    if (b.aux) {
+        cudaStreamSynchronize(b.aux);
+        cudaStreamDestroy(b.aux);
+    }
+    if (b.ev_fork) cudaEventDestroy(b.ev_fork);
+    if (b.ev_join) cudaEventDestroy(b.ev_join);
     if (b.stage) cudaFreeHost(b.stage);
     for (cudaEvent_t e : b.stage_ev)
         if (e) cudaEventDestroy(e);

@@ -28,14 +28,16 @@ void launch_perp_pair(cudaStream_t s, const ErrParams& ep, uint64_t seed, int64_
                       uint64_t cycle, double ratio, double* xi, double* nu, int* foffs,
                       double* scal, const int* err, int M);
 void launch_gather_cz(cudaStream_t s, int M, const double* scal, double* cz);
+// errors (E_BETA / E_ALPHA) go to aerr; launch_merge_err folds them into err after the
+// pull chain joined, so an earlier-stage error keeps precedence
 void launch_barrier_alpha(cudaStream_t s, const double* cz_all, int n_total, int M, double n_psi,
-                          int one_stage,
-                          double* scal, double* wb, int* err);
+                          int one_stage, double* scal, double* wb, int* aerr);
+void launch_merge_err(cudaStream_t s, int M, const int* aerr, int* err);
 void launch_local_blocks(cudaStream_t s, const ErrParams& ep, const double* xi, const double* nu,
                          const double* scal, const double* wb, const int* cells, int n_obs,
                          const int* order, const int* level_start, int n_levels,
-                         const int* foffs, const double* usig, double* z, const int* err, int M,
-                         int one_stage);
+                         const int* foffs, const double* usig, double* z, const int* err,
+                         const int* aerr, int M, int one_stage);
 void launch_drifters(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
                      const float* hv, int M, int n_d, double dt, double* pos, int* wind, int* err,
                      int* err_pos);
