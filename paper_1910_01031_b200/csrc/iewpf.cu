@@ -237,6 +237,33 @@ pull_tables_kernel(SweParams sp, ErrParams ep, const int4* __restrict__ lists,
         const int db = wrapf(b - bo + WH, nyc);
         return (db < WIN ? db : WP - 1) * WP;
     });
+    __syncthreads();  // the tables above are global memory written by warps 0-2
+    // the window's reach inside the tile: column groups / row groups with at least one of
+    // their four coarse points inside the 11x11 window (the others interpolate to exactly 0)
+    if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        bool ca_ = false, ra_ = false;
+        if (l < T.ncg)
+            for (int q = 0; q < 4; ++q) ca_ |= T.cg_a[l][q] != WP - 1;
+        if (l < T.nrg)
+            for (int q = 0; q < 4; ++q) ra_ |= T.brow[T.rg_sl[l][q]] != (WP - 1) * WP;
+        const unsigned bc = __ballot_sync(0xffffffffu, ca_), br = __ballot_sync(0xffffffffu, ra_);
+        if (l == 0) {
+            if (bc && br) {
+                const int gc0 = __ffs(bc) - 1, gc1 = 31 - __clz(bc);
+                const int gr0 = __ffs(br) - 1, gr1 = 31 - __clz(br);
+                T.c0 = T.cg_first[gc0];
+                T.c1 = T.cg_first[gc1 + 1] - 1;
+                T.r0 = T.rg_first[gr0];
+                T.r1 = T.rg_first[gr1 + 1] - 1;
+            } else {
+                T.r0 = 1;
+                T.r1 = 0;
+                T.c0 = 1;
+                T.c1 = 0;
+            }
+        }
+    }
 }
 
 __global__ void __launch_bounds__(tile::NT, DC_PULL_MIN_BLOCKS)
@@ -296,8 +323,23 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
         asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
         const bool more = li + 1 < cnt;
-        tile::interpolate(
-            S, [&](int brow, int a) { return W[brow + a]; },
+        // the window's reach in this tile (halo coordinates); outside it the pull is an
+        // exact zero, whose add leaves the float state unchanged
+        const int r0 = S.t.r0, r1 = S.t.r1, c0 = S.t.c0, c1 = S.t.c1;
+        if (r0 > r1) {  // out of reach: nothing to add; prefetch the next entry
+            __syncthreads();  // every thread has read the box before the tables are reused
+            if (more) {
+                load_win(li + 1);
+                load_tab(li + 1);
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+            continue;
+        }
+        // D on the reach + 2 (the geostrophic differences of the cells next to it read one
+        // more D), applied on the reach + 1
+        tile::interpolate_box(
+            S, max(r0 - 2, 0), min(r1 + 2, tile::YH - 1), max(c0 - 2, 0),
+            min(c1 + 2, tile::XW - 1), [&](int brow, int a) { return W[brow + a]; },
             [&] {  // pass 1 done: the window is free, fetch the next observation's
                 if (more) load_win(li + 1);
             },
@@ -305,11 +347,15 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
                 if (more) load_tab(li + 1);
                 asm volatile("cp.async.commit_group;\n" ::);
             });
+        const int ar0 = max(r0 - 1, 1), ar1 = min(r1 + 1, TY);
+        const int ac0 = max(c0 - 1, 1), ac1 = min(c1 + 1, TX);
+        const bool colin = tx + 1 >= ac0 && tx + 1 <= ac1;
 #pragma unroll
         for (int q = 0; q < kRowsPerThread; ++q) {
             const int r = ty + kWarps * q, k = k0 + r;
             if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
             const int rr = r + 1, jl = tx + 1;
+            if (!colin || rr < ar0 || rr > ar1) continue;
             const double de = S.D[rr][jl];
             const double dhu = -cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
             const double dhv = cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);

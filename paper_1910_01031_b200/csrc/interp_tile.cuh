@@ -43,6 +43,10 @@ struct Tab {
     int rg_first[YH + 1];    // first halo row of each row group (+ end sentinel)
     int brow[NBMAX];         // coarse row of each X slot (mapped)
     int nb, ncg, nrg;
+    // IEWPF pull only (pull_tables): halo rows / columns where the interpolated field can be
+    // non-zero (the observation's 11x11 window reaches them), [r0, r1] x [c0, c1]; r0 > r1
+    // when the tile is outside the window's reach
+    int r0, r1, c0, c1;
 };
 struct alignas(16) TabA : Tab {};  // 16-byte aligned, copied with 16-byte cp.async
 constexpr int kTabChunks = (sizeof(TabA) + 15) / 16;
@@ -189,6 +193,46 @@ __device__ __forceinline__ void setup(Smem& S, const ErrParams& ep, int nx, int 
 struct NoHook {
     __device__ __forceinline__ void operator()() const {}
 };
+
+// Passes 1 and 2 restricted to a box (pull_apply): X for the column groups meeting halo
+// columns [ca, cb], D for the row groups meeting halo rows [ra, rb] and columns [ca, cb].
+// Outside the observation's reach the interpolated field is exactly zero, so a caller that
+// needs D on a box around the reach computes exactly the values the full passes would.
+template <class VALF, class H1 = NoHook, class H2 = NoHook>
+__device__ __forceinline__ void interpolate_box(Smem& S, int ra, int rb, int ca, int cb,
+                                                VALF valf, H1 after1 = H1{},
+                                                H2 after2 = H2{}) {
+    const Tab& T = S.t;
+    const int tid = threadIdx.x;
+    // column groups meeting [ca, cb]: g0 .. g1
+    int g0 = 0, g1 = T.ncg - 1;
+    while (g0 < g1 && T.cg_first[g0 + 1] <= ca) ++g0;
+    while (g1 > g0 && T.cg_first[g1] > cb) --g1;
+    const int ncg = g1 - g0 + 1, n1 = T.nb * ncg;
+    for (int i = tid; i < n1; i += NT) {  // (X slot, column group)
+        const int s = i / ncg, g = g0 + (i - s * ncg);
+        const int b = T.brow[s];
+        const Cm m = coef(valf(b, T.cg_a[g][0]), valf(b, T.cg_a[g][1]), valf(b, T.cg_a[g][2]),
+                          valf(b, T.cg_a[g][3]));
+        const int j1 = T.cg_first[g + 1];
+        for (int jl = T.cg_first[g]; jl < j1; ++jl) S.X[s][jl] = eval(m, T.ct[jl]);
+    }
+    __syncthreads();
+    after1();
+    int h0 = 0, h1 = T.nrg - 1;
+    while (h0 < h1 && T.rg_first[h0 + 1] <= ra) ++h0;
+    while (h1 > h0 && T.rg_first[h1] > rb) --h1;
+    const int w = cb - ca + 1, n2 = (h1 - h0 + 1) * w;
+    for (int i = tid; i < n2; i += NT) {  // (row group, halo column)
+        const int g = h0 + i / w, jl = ca + (i - (g - h0) * w);
+        const Cm m = coef(S.X[T.rg_sl[g][0]][jl], S.X[T.rg_sl[g][1]][jl], S.X[T.rg_sl[g][2]][jl],
+                          S.X[T.rg_sl[g][3]][jl]);
+        const int r1 = T.rg_first[g + 1];
+        for (int r = T.rg_first[g]; r < r1; ++r) S.D[r][jl] = eval(m, T.rt[r]);
+    }
+    __syncthreads();
+    after2();
+}
 
 // Passes 1 and 2 into S.D from the tables in S.t. VALF(mapped row, mapped col) returns the
 // coarse value. Ends with a barrier. after1 runs right after the barrier that ends pass 1
