@@ -62,6 +62,10 @@ struct StepCtl {
     int* any_active;    // loop condition (host-visible in the fallback path)
     unsigned* mdone;    // [M] stage-2 CTAs of the member finished this substep (fused end)
     int* n_active;      // members still stepping (fused end: the last one ends the loop)
+    unsigned* step_max; // max substeps of a member in the step in progress
+    unsigned long long* iters;  // [0] += substep-loop iterations per step (max over members),
+                                // [1] += member-substeps (cell-updates / cells), counted as
+                                // members retire from a step
 };
 
 struct ErrParams {

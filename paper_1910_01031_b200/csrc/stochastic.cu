@@ -218,6 +218,27 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
         eta[o] = fe;
         hu[o] = fu;
         hv[o] = fv;
+        // the periodic ghost frame: cells within 2 of an edge also go to
+        // their ghost copies, so the next model step needs no fix_ghosts pass
+        const int kk = k0 + rr - 1;
+        const ptrdiff_t gc = j < 2 ? sp.nx : (j >= sp.nx - 2 ? -sp.nx : 0);
+        const ptrdiff_t gr = kk < 2 ? sp.ny : (kk >= sp.ny - 2 ? -sp.ny : 0);
+        if (gc) {
+            eta[o + gc] = fe;
+            hu[o + gc] = fu;
+            hv[o + gc] = fv;
+        }
+        if (gr) {
+            const ptrdiff_t g = gr * static_cast<ptrdiff_t>(pitch);
+            eta[o + g] = fe;
+            hu[o + g] = fu;
+            hv[o + g] = fv;
+            if (gc) {
+                eta[o + g + gc] = fe;
+                hu[o + g + gc] = fu;
+                hv[o + g + gc] = fv;
+            }
+        }
         if (mx) {  // load() statistics of the new state, IEEE float (swe.hpp:307-316)
             const float h = __fadd_rn(sp.H, fe);
             mn_h = fminf(mn_h, h);
