@@ -480,12 +480,11 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         choose_strips(ctx->sp, sms, swe_stage_occupancy());
     }
-    // CTA rows of the stage grid (members x strips, plus two tail strips per member) must
-    // fit gridDim.y
-    if (static_cast<long long>(ctx->M) * (ctx->sp.strips + 2) > 65535)
+    // per-member kernels put the member index in gridDim.y / z (<= 65535)
+    if (ctx->M > 65535)
         return set_err(ctx, DC_EINVAL,
-                       "too many members for one context (members x strips > 65535): split "
-                       "them over several contexts / GPUs");
+                       "too many members for one context (> 65535): split them over several "
+                       "contexts / GPUs");
     {
         // two short strips of ~2/5 of a big strip per member (measured 2.6 % per model
         // step at 500x300 x 100 members against uniform strips)

@@ -40,6 +40,8 @@ struct SweParams {
     const int2* units;    // optional CTA row units {m, y0 | y1 << 16}: big strips first,
     int n_units;          // short ones last so the final wave drains quickly (api.cu)
     int ctas_per_member;  // stage-2 CTAs of one member (set per launch by launch_stage)
+    int tiles_x;          // 252-column tiles per row (set per launch)
+    int grid_units;       // row units of the launch (grid y, continued in z past 65535)
     int end_mode;         // stage 2: fused substep end (0 off, 1 flag only, 2 + graph cond)
     unsigned long long end_cond;  // cudaGraphConditionalHandle of the step's while node
     float H, g, theta, cf_x, cf_y, inv_g, idx, idy, fH;

@@ -414,3 +414,23 @@ def test_failed_member_recovers_when_overwritten(oracle):
     ens.model_step(1)
     ens.sync()
     ens.close()
+
+
+@pytest.mark.timeout(600)
+def test_many_members_one_context(oracle):
+    """5100 members of the 500x300 jet in one context (members x strips > 65535, the old
+    gridDim.y cliff of the stage grid; the stage grid is 1-D now): one model step, the
+    first and last members bitwise equal to the oracle."""
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair()
+    n = 5100
+    ens = Ensemble(cfg, n)
+    ens.init_double_jet()
+    ens.model_step(1)
+    s = oracle.init_double_jet(p)
+    oracle.model_step(p, s, 1)
+    for m in (0, n - 1):
+        e, u, v, t = ens.download_member(m)
+        assert np.array_equal(e, s.eta) and np.array_equal(u, s.hu) and np.array_equal(v, s.hv)
+        assert t == 60.0
+    ens.close()
