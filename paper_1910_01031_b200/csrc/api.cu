@@ -46,6 +46,7 @@ struct dc_ctx {
     float* blk[2] = {nullptr};  // the two state sets (psi^n, psi*), 3 fields each
     float* f[6] = {nullptr};  // eta, hu, hv, stage eta, stage hu, stage hv (views into blk)
     CUtensorMap maps[2];      // TMA maps of the two state sets (stage kernels)
+    CUtensorMap qmap;         // state set 0, box of one 32x30 tile + halo (tile kernels)
     StepCtl ctl{};
     void* ctl_mem = nullptr;
     unsigned long long* substep_iters = nullptr; // device counters (graph path): [iters, member-substeps]
@@ -373,7 +374,7 @@ void apply_q_half_with_stats(dc_ctx* ctx, const int* offsets, double scale,
         launch_reset_stats(ctx->stream, ctx->sp, ctx->ctl);
         ctx->launches += 1;
     }
-    launch_q_half_apply(ctx->stream, ctx->sp, ctx->ep, ctx->corr, offsets, scale, ctx->f[0],
+    launch_q_half_apply(ctx->stream, &ctx->qmap, ctx->sp, ctx->ep, ctx->corr, offsets, scale, ctx->f[0],
                         ctx->f[1], ctx->f[2], ctx->ctl.err, ctx->ctl.err_pos, ctx->M,
                         ctx->ctl.mx, prof_name);
     ctx->stats = 1;
@@ -517,6 +518,8 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
         if (!make_state_map(&ctx->maps[s], ctx->blk[s], ctx->sp, ctx->field_elems))
             return set_err(ctx, DC_ECUDA, "cuTensorMapEncodeTiled failed for the state maps");
     }
+    if (!make_state_map(&ctx->qmap, ctx->blk[0], ctx->sp, ctx->field_elems, 36, 30))
+        return set_err(ctx, DC_ECUDA, "cuTensorMapEncodeTiled failed for the tile map");
     const int M = ctx->M;
     // 17 arrays, each rounded up to 16 bytes by take()
     size_t bytes = 17 * ((static_cast<size_t>(M) * 4 * sizeof(double) + 15) / 16 * 16) + 64;

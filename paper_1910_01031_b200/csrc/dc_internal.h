@@ -131,10 +131,12 @@ void launch_philox_soar(cudaStream_t s, const ErrParams& ep, int M, uint64_t see
                         int* offsets, const int* err);
 void launch_coarse_soar(cudaStream_t s, const ErrParams& ep, int M, const double* in,
                         double* out, const int* err);
-void launch_q_half_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
-                         const double* corr, const int* offsets, double scale, float* eta,
-                         float* hu, float* hv, int* err, int* err_pos, int M,
-                         unsigned* mx = nullptr, const char* prof_name = "q_half_apply");
+// smap: the model state set's TMA map with box {tile::TX + 4, tile::TY, 3} (api.cu qmap)
+void launch_q_half_apply(cudaStream_t s, const CUtensorMap* smap, const SweParams& sp,
+                         const ErrParams& ep, const double* corr, const int* offsets,
+                         double scale, float* eta, float* hu, float* hv, int* err,
+                         int* err_pos, int M, unsigned* mx = nullptr,
+                         const char* prof_name = "q_half_apply");
 
 // swe.cu launchers
 void launch_cfl_scan(cudaStream_t s, const SweParams& sp, const float* eta, const float* hu,
@@ -144,9 +146,9 @@ void launch_step_begin(cudaStream_t s, const SweParams& sp, StepCtl ctl,
 void launch_reset_stats(cudaStream_t s, const SweParams& sp, StepCtl ctl);
 int swe_stage_occupancy();
 // TMA map of a state set (3 fields field_stride floats apart, origin = storage row -2 of
-// member 0, column -2)
+// member 0, column -2); box {box_cols, box_rows, 3} (0: the stage kernels' {256, 3})
 bool make_state_map(CUtensorMap* map, const float* origin, const SweParams& sp,
-                    size_t field_stride);
+                    size_t field_stride, int box_cols = 0, int box_rows = 0);
 // refresh the ghost frame of a state set (f0 = field 0 at cell (0, 0))
 void launch_fix_ghosts(cudaStream_t s, const SweParams& sp, float* f0, size_t field_stride);
 // One SSP-RK2 stage over every member. maps: [0] the input state set, [1] the psi^n set

@@ -25,6 +25,7 @@
 #include "detmath.cuh"
 #include "iewpf_kernels.h"
 #include "interp_tile.cuh"
+#include "tma.cuh"
 
 namespace dcg {
 
@@ -196,11 +197,6 @@ constexpr int WP = 16;  // padded window pitch: indices 11..15 read exact zeros
 using tile::kRowsPerThread;
 using tile::kWarps;
 
-__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
-}
-
 #ifndef DC_PULL_MIN_BLOCKS
 #define DC_PULL_MIN_BLOCKS 6
 #endif
@@ -266,14 +262,18 @@ pull_tables_kernel(SweParams sp, ErrParams ep, const int4* __restrict__ lists,
     }
 }
 
+constexpr int kStw = TX + 4;  // TMA box width: cells j0-2 .. j0+TX+1 (16-byte aligned start)
+
 __global__ void __launch_bounds__(tile::NT, DC_PULL_MIN_BLOCKS)
-pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, int n_obs,
+pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrParams ep,
+                  const double* __restrict__ win, int n_obs,
                   const int4* __restrict__ lists, const int* __restrict__ counts, int tiles_x,
                   const tile::TabA* __restrict__ tabs, float* eta, float* hu, float* hv,
                   int* err, int* err_pos) {
     __shared__ double W[WP * WP];
     __shared__ tile::Smem S;
-    __shared__ float ST[3][TY][TX];  // the tile's state across all observations
+    __shared__ alignas(128) float ST[3][TY][kStw];  // the tile's state across all observations
+    __shared__ alignas(8) unsigned long long bar;
     const int m = blockIdx.y;
     // another tile of the member may raise E_DRY_ADD meanwhile: decide once per CTA
     if (__syncthreads_or(err[m] != 0)) return;
@@ -284,17 +284,15 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const int j = j0 + tx;
     const size_t mbase = static_cast<size_t>(m) * sp.mstride;
-    // each thread stages (and later owns) its cells in shared memory: registers stay free
-    // for occupancy, and no barrier is needed since only the owner touches them
-#pragma unroll
-    for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = ty + kWarps * q, k = k0 + r;
-        if (r < TY && k < sp.ny && j < sp.nx) {
-            const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
-            cp_async4(&ST[0][r][tx], eta + o);
-            cp_async4(&ST[1][r][tx], hu + o);
-            cp_async4(&ST[2][r][tx], hv + o);
-        }
+    // the tile's state arrives in shared memory by one TMA box (cells j0-2 .. j0+TX+1, TY
+    // rows, 3 fields) and stays there across all the tile's observations; each thread then
+    // owns its cells, so the fold needs no further barrier for them
+    const uint32_t b = smem_u32(&bar);
+    if (tid == 0) {
+        mbar_init(b, 1);
+        mbar_fence_init();
+        mbar_expect_tx(b, sizeof(ST));
+        tma_row(smem_u32(&ST[0][0][0]), &smap, j0, m * (sp.ny + 4) + 2 + k0, b);
     }
     // the window pad stays zero: the copies below touch only da, db < WIN
     for (int i = tid; i < WP * WP; i += tile::NT) W[i] = 0.0;
@@ -318,8 +316,9 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
     bool dry = false;
     int dry_at = 0x7fffffff;
     const double cy = ep.cy, cx = ep.cx, heq = ep.h_eq;
+    mbar_wait(b, 0);  // the tile state
     for (int li = 0; li < cnt; ++li) {
-        // entry li's window and tables (and, at li = 0, the tile state) have landed
+        // entry li's window and tables have landed
         asm volatile("cp.async.wait_group 0;\n" ::);
         __syncthreads();
         const bool more = li + 1 < cnt;
@@ -359,14 +358,14 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
             const double de = S.D[rr][jl];
             const double dhu = -cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
             const double dhv = cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
-            const double ee = static_cast<double>(ST[0][r][tx]) + 1.0 * de;
+            const double ee = static_cast<double>(ST[0][r][tx + 2]) + 1.0 * de;
             if (!(heq + ee > 0.0)) {
                 dry = true;
                 dry_at = min(dry_at, k * sp.nx + j);
             }
-            ST[0][r][tx] = static_cast<float>(ee);
-            ST[1][r][tx] = static_cast<float>(static_cast<double>(ST[1][r][tx]) + 1.0 * dhu);
-            ST[2][r][tx] = static_cast<float>(static_cast<double>(ST[2][r][tx]) + 1.0 * dhv);
+            ST[0][r][tx + 2] = static_cast<float>(ee);
+            ST[1][r][tx + 2] = static_cast<float>(static_cast<double>(ST[1][r][tx + 2]) + 1.0 * dhu);
+            ST[2][r][tx + 2] = static_cast<float>(static_cast<double>(ST[2][r][tx + 2]) + 1.0 * dhv);
         }
     }
 #pragma unroll
@@ -374,9 +373,9 @@ pull_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ win, in
         const int r = ty + kWarps * q, k = k0 + r;
         if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
         const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
-        eta[o] = ST[0][r][tx];
-        hu[o] = ST[1][r][tx];
-        hv[o] = ST[2][r][tx];
+        eta[o] = ST[0][r][tx + 2];
+        hu[o] = ST[1][r][tx + 2];
+        hv[o] = ST[2][r][tx + 2];
     }
     if (dry) {
         atomicCAS(err + m, 0, E_DRY_ADD);
@@ -720,7 +719,8 @@ void launch_tile_lists(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
 
 size_t pull_table_bytes() { return sizeof(tile::TabA); }
 
-void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep, const double* win,
+void launch_pull_apply(cudaStream_t s, const CUtensorMap* smap, const SweParams& sp,
+                       const ErrParams& ep, const double* win,
                        const int* cells, int n_obs, const int* lists, const int* counts,
                        int n_tiles, int tiles_x, void* tabs, float* eta, float* hu, float* hv,
                        int* err, int* err_pos, int M, double entries, double touched_cells) {
@@ -734,7 +734,7 @@ void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
     // window once, the tables once
     KScope ks(s, "pull_apply", (24.0 * touched_cells + 8.0 * WIN * WIN * n_obs) * M +
                                    entries * sizeof(tile::TabA));
-    pull_apply_kernel<<<dim3(n_tiles, M), tile::NT, 0, s>>>(sp, ep, win, n_obs,
+    pull_apply_kernel<<<dim3(n_tiles, M), tile::NT, 0, s>>>(*smap, sp, ep, win, n_obs,
                                                        reinterpret_cast<const int4*>(lists), counts,
                                                        tiles_x, T, eta, hu, hv, err, err_pos);
 }

@@ -20,7 +20,8 @@ void launch_tile_lists(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
 // pull_tables (member-independent interpolation tables of every (tile, covering obs),
 // tabs: n_tiles x n_obs x pull_table_bytes()) + pull_apply
 size_t pull_table_bytes();
-void launch_pull_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep, const double* win,
+void launch_pull_apply(cudaStream_t s, const CUtensorMap* smap, const SweParams& sp,
+                       const ErrParams& ep, const double* win,
                        const int* cells, int n_obs, const int* lists, const int* counts,
                        int n_tiles, int tiles_x, void* tabs, float* eta, float* hu, float* hv,
                        int* err, int* err_pos, int M, double entries, double touched_cells);

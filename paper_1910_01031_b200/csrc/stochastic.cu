@@ -21,6 +21,7 @@
 #include "detmath.cuh"
 #include "fp32_rn.cuh"
 #include "interp_tile.cuh"
+#include "tma.cuh"
 
 namespace dcg {
 
@@ -132,11 +133,6 @@ philox_soar_kernel(ErrParams ep, int M, uint64_t seed, uint64_t tag, long long m
 using tile::TX;
 using tile::TY;
 
-__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
-}
-
 __device__ __forceinline__ unsigned ordered_bits(float f) {
     const unsigned b = __float_as_uint(f);
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
@@ -151,13 +147,21 @@ using tile::kWarps;
 #define DC_QHALF_MIN_BLOCKS 6
 #endif
 
+// The tile's state arrives by TMA: one box {TX+4 columns from cell j0-2, TY rows, 3 fields}
+// of the state set's map (storage column j0 is 16-byte aligned; the box's first two and
+// last two columns are not used).
+constexpr int kStw = TX + 4;
+static_assert(kStw * sizeof(float) % 16 == 0, "TMA box rows must be 16-byte multiples");
+
 __global__ void __launch_bounds__(tile::NT, DC_QHALF_MIN_BLOCKS)
-q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
-                    const int* __restrict__ offsets, double scale, float* eta, float* hu,
-                    float* hv, int* err, int* err_pos, unsigned* mx) {
+q_half_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrParams ep,
+                    const double* __restrict__ corr, const int* __restrict__ offsets,
+                    double scale, float* eta, float* hu, float* hv, int* err, int* err_pos,
+                    unsigned* mx) {
     __shared__ tile::Smem S;
-    __shared__ float ST[3][TY][TX];
+    __shared__ alignas(128) float ST[3][TY][kStw];
     __shared__ float red[3][kWarps];
+    __shared__ alignas(8) unsigned long long bar;
     const int m = blockIdx.z;
     // another tile of the member may raise E_DRY_ADD meanwhile: decide once per CTA
     if (__syncthreads_or(err[m] != 0)) return;
@@ -168,75 +172,68 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
     // this thread's cells: column j, rows k0 + ty + 8q
     const size_t cell0 = static_cast<size_t>(m) * sp.mstride + static_cast<size_t>(k0 + ty) * pitch + j;
     const size_t step = static_cast<size_t>(kWarps) * pitch;
-    bool okq[kRowsPerThread];
-#pragma unroll
-    for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = ty + kWarps * q;
-        okq[q] = (r < TY) && (k0 + r < sp.ny) && (j < sp.nx);
+    const uint32_t b = smem_u32(&bar);
+    if (threadIdx.x == 0) {
+        mbar_init(b, 1);
+        mbar_fence_init();
+        mbar_expect_tx(b, sizeof(ST));
+        // storage row of cell row k0 of member m (the map starts at row -2 of member 0)
+        tma_row(smem_u32(&ST[0][0][0]), &smap, j0, m * (sp.ny + 4) + 2 + k0, b);
     }
-    // stage the tile's state in shared memory with cp.async first: the loads' latency
-    // overlaps the interpolation passes without holding registers
-#pragma unroll
-    for (int q = 0; q < kRowsPerThread; ++q) {
-        if (!okq[q]) continue;
-        const size_t o = cell0 + q * step;
-        const int r = ty + kWarps * q;
-        cp_async4(&ST[0][r][tx], eta + o);
-        cp_async4(&ST[1][r][tx], hu + o);
-        cp_async4(&ST[2][r][tx], hv + o);
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
     const int oj = offsets[2 * m], ok = offsets[2 * m + 1];
     const double* cf = corr + static_cast<size_t>(m) * ep.nxc * ep.nyc;
     const int nxc = ep.nxc;
     tile::setup(S, ep, sp.nx, sp.ny, j0, k0, oj, ok, [](int a) { return a; },
-                [&](int b) { return b * nxc; });
+                [&](int bb) { return bb * nxc; });  // (its barrier publishes the mbarrier)
     tile::interpolate(S, [&](int brow, int a) { return __ldg(cf + brow + a); });
     // geostrophic balance (stochastic.hpp:122-139) + add in fp64, cast to float
     bool dry = false;
     int dry_at = 0x7fffffff;
     float mx_u = 0.0f, mx_v = 0.0f, mn_h = 3.402823466e+38f;
     const double cy = ep.cy, cx = ep.cx, heq = ep.h_eq;
-    asm volatile("cp.async.wait_group 0;\n" ::);  // own copies only: no barrier needed
+    mbar_wait(b, 0);
+    // cells within 2 of a domain edge also go to their ghost copies, so the
+    // next model step needs no fix_ghosts pass; interior tiles skip that (uniform branch)
+    const bool edge = j0 < 2 || j0 + TX > sp.nx - 2 || k0 < 2 || k0 + TY > sp.ny - 2;
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
-        if (!okq[q]) continue;
-        const int rr = ty + kWarps * q + 1, jl = tx + 1;
+        const int r = ty + kWarps * q;
+        if (!((r < TY) && (k0 + r < sp.ny) && (j < sp.nx))) continue;
+        const int rr = r + 1, jl = tx + 1;
         const double de = S.D[rr][jl];
         const double dhu = -cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
         const double dhv = cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
-        const int r = rr - 1;
-        const double e = static_cast<double>(ST[0][r][tx]) + scale * de;
+        const double e = static_cast<double>(ST[0][r][tx + 2]) + scale * de;
         if (!(heq + e > 0.0)) {
             dry = true;
-            dry_at = min(dry_at, (k0 + rr - 1) * sp.nx + j);
+            dry_at = min(dry_at, (k0 + r) * sp.nx + j);
         }
         const float fe = static_cast<float>(e);
-        const float fu = static_cast<float>(static_cast<double>(ST[1][r][tx]) + scale * dhu);
-        const float fv = static_cast<float>(static_cast<double>(ST[2][r][tx]) + scale * dhv);
+        const float fu = static_cast<float>(static_cast<double>(ST[1][r][tx + 2]) + scale * dhu);
+        const float fv = static_cast<float>(static_cast<double>(ST[2][r][tx + 2]) + scale * dhv);
         const size_t o = cell0 + q * step;
         eta[o] = fe;
         hu[o] = fu;
         hv[o] = fv;
-        // the periodic ghost frame: cells within 2 of an edge also go to
-        // their ghost copies, so the next model step needs no fix_ghosts pass
-        const int kk = k0 + rr - 1;
-        const ptrdiff_t gc = j < 2 ? sp.nx : (j >= sp.nx - 2 ? -sp.nx : 0);
-        const ptrdiff_t gr = kk < 2 ? sp.ny : (kk >= sp.ny - 2 ? -sp.ny : 0);
-        if (gc) {
-            eta[o + gc] = fe;
-            hu[o + gc] = fu;
-            hv[o + gc] = fv;
-        }
-        if (gr) {
-            const ptrdiff_t g = gr * static_cast<ptrdiff_t>(pitch);
-            eta[o + g] = fe;
-            hu[o + g] = fu;
-            hv[o + g] = fv;
+        if (edge) {
+            const int kk = k0 + r;
+            const ptrdiff_t gc = j < 2 ? sp.nx : (j >= sp.nx - 2 ? -sp.nx : 0);
+            const ptrdiff_t gr = kk < 2 ? sp.ny : (kk >= sp.ny - 2 ? -sp.ny : 0);
             if (gc) {
-                eta[o + g + gc] = fe;
-                hu[o + g + gc] = fu;
-                hv[o + g + gc] = fv;
+                eta[o + gc] = fe;
+                hu[o + gc] = fu;
+                hv[o + gc] = fv;
+            }
+            if (gr) {
+                const ptrdiff_t g = gr * static_cast<ptrdiff_t>(pitch);
+                eta[o + g] = fe;
+                hu[o + g] = fu;
+                hv[o + g] = fv;
+                if (gc) {
+                    eta[o + g + gc] = fe;
+                    hu[o + g + gc] = fu;
+                    hv[o + g + gc] = fv;
+                }
             }
         }
         if (mx) {  // load() statistics of the new state, IEEE float (swe.hpp:307-316)
@@ -253,26 +250,26 @@ q_half_apply_kernel(SweParams sp, ErrParams ep, const double* __restrict__ corr,
         atomicMin(err_pos + m, dry_at);
     }
     if (mx) {
-        for (int o = 16; o > 0; o >>= 1) {
-            mx_u = fmaxf(mx_u, __shfl_xor_sync(0xffffffffu, mx_u, o));
-            mx_v = fmaxf(mx_v, __shfl_xor_sync(0xffffffffu, mx_v, o));
-            mn_h = fminf(mn_h, __shfl_xor_sync(0xffffffffu, mn_h, o));
-        }
+        // warp maxima / minimum in one CREDUX each (order-free: max / min are exact)
+        float a_, b_, c_;
+        asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(a_) : "f"(mx_u));
+        asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(b_) : "f"(mx_v));
+        asm("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(c_) : "f"(mn_h));
         if (tx == 0) {
-            red[0][ty] = mx_u;
-            red[1][ty] = mx_v;
-            red[2][ty] = mn_h;
+            red[0][ty] = a_;
+            red[1][ty] = b_;
+            red[2][ty] = c_;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-            float a = red[0][0], b = red[1][0], c = red[2][0];
+            float a = red[0][0], bb = red[1][0], c = red[2][0];
             for (int i = 1; i < kWarps; ++i) {
                 a = fmaxf(a, red[0][i]);
-                b = fmaxf(b, red[1][i]);
+                bb = fmaxf(bb, red[1][i]);
                 c = fminf(c, red[2][i]);
             }
             atomicMax(mx + 4 * m + 0, __float_as_uint(a));
-            atomicMax(mx + 4 * m + 1, __float_as_uint(b));
+            atomicMax(mx + 4 * m + 1, __float_as_uint(bb));
             atomicMin(mx + 4 * m + 2, ordered_bits(c));
         }
     }
@@ -307,16 +304,16 @@ void launch_coarse_soar(cudaStream_t s, const ErrParams& ep, int M, const double
     coarse_soar_kernel<<<dim3((nr + 255) / 256, M), 256, 0, s>>>(ep, M, in, out, err);
 }
 
-void launch_q_half_apply(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
-                         const double* corr, const int* offsets, double scale, float* eta,
-                         float* hu, float* hv, int* err, int* err_pos, int M, unsigned* mx,
-                         const char* prof_name) {
+void launch_q_half_apply(cudaStream_t s, const CUtensorMap* smap, const SweParams& sp,
+                         const ErrParams& ep, const double* corr, const int* offsets,
+                         double scale, float* eta, float* hu, float* hv, int* err,
+                         int* err_pos, int M, unsigned* mx, const char* prof_name) {
     dim3 grid((sp.nx + TX - 1) / TX, (sp.ny + TY - 1) / TY, M);
     // the state read and written once (24 B/cell) + the coarse field
     KScope ks(s, prof_name,
               (24.0 * sp.nx * sp.ny + 8.0 * ep.nxc * ep.nyc) * M);
-    q_half_apply_kernel<<<grid, tile::NT, 0, s>>>(sp, ep, corr, offsets, scale, eta, hu, hv, err,
-                                             err_pos, mx);
+    q_half_apply_kernel<<<grid, tile::NT, 0, s>>>(*smap, sp, ep, corr, offsets, scale, eta, hu,
+                                                  hv, err, err_pos, mx);
 }
 
 } // namespace dcg
