@@ -189,9 +189,11 @@ def load_peaks():
         return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-# FP32 lane operations per cell of the exact stage kernels, counted from their SASS
-# (FFMA2/FADD2/FMUL2 = 2, FFMA/FADD/FMUL = 1; tools/sass_hist.py): stage 1, stage 2
-FP32_OPS_PER_CELL = (208.0, 229.0)
+# FP32 lane operations per cell of the exact stage kernels: predicated-on FFMA2/FADD2/FMUL2
+# (2 each) + FFMA/FADD/FMUL (1) executed per member cell in the ncu source page of
+# profiles/r2_swe_stage_ncu.json (215.6 / 238.1 at 1000x600), less the 256-for-252-column
+# window halo (x 1000/1024): the work one output cell needs. Stage 1, stage 2.
+FP32_OPS_PER_CELL = (210.5, 232.5)
 
 # cycle stages ("stage shares") of every kernel name the profiler reports
 STAGE_OF = {
