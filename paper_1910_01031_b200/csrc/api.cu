@@ -430,19 +430,28 @@ dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base
     return st;
 }
 
-// Strip height of the SWE stage grid: balance the y-halo overhead (~0.45 rows of extra
-// work per strip-row) against the wave quantisation of
-// (x tiles x members x strips) CTAs over SMs x 3 resident CTAs.
+// Strip height of the SWE stage grid: balance the y prologue of a strip (the two rows
+// above it are loaded and reconstructed again: ~1.4 rows of work per strip, measured)
+// against wave quantisation of (x tiles x members x strips) CTAs over SMs x resident
+// CTAs -- softened when there are many waves, since each member's two short tail strips
+// fill the last one.
+// Measured at 1000x600: 1000 members 154.9 / 153.8 / 152.2 ms per model step at 47 / 64 /
+// 120-row strips; 125 members 19.90 / 19.67 / 19.57 at 40 / 86 / 120; at 500x300 x 100
+// members 28 rows stays best (86: +14 %, 120: +28 %: too few CTAs to fill the waves).
 static void choose_strips(SweParams& P, int sms, int per_sm) {
     const int xt = (P.nx + 251) / 252;
     const double slots = static_cast<double>(sms) * per_sm;
     double best = 1e30;
-    for (int s = std::max(1, (P.ny + 63) / 64); s <= std::max(1, (P.ny + 7) / 8); ++s) {
+    for (int s = std::max(1, (P.ny + 255) / 256); s <= std::max(1, (P.ny + 7) / 8); ++s) {
         const int by = (P.ny + s - 1) / s;
         const int strips = (P.ny + by - 1) / by;
         const double n = static_cast<double>(xt) * P.M * strips;
         const double waves = n / slots;
-        const double cost = std::ceil(waves) / waves * (1.0 + 0.45 / by);
+        // few waves: a partial last wave idles SMs outright; many waves: the tail strips
+        // absorb most of it
+        const double quant = waves < 8.0 ? std::ceil(waves) / waves
+                                         : 1.0 + 0.3 * (std::ceil(waves) - waves) / waves;
+        const double cost = quant * (1.0 + 1.4 / by);
         if (cost < best - 1e-9) {
             best = cost;
             P.by = by;
