@@ -485,10 +485,14 @@ static std::vector<int2> build_units(const SweParams& P, int tail_rows, int n_ta
 
 static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
     CU(cudaSetDevice(device));
+    double stage_waves = 0.0;  // waves of big strips in one stage launch
     {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-        choose_strips(ctx->sp, sms, swe_stage_occupancy());
+        const int per_sm = swe_stage_occupancy();
+        choose_strips(ctx->sp, sms, per_sm);
+        stage_waves = static_cast<double>((ctx->sp.nx + 251) / 252) * ctx->M * ctx->sp.strips /
+                      (static_cast<double>(sms) * per_sm);
     }
     // per-member kernels put the member index in gridDim.y / z (<= 65535)
     if (ctx->M > 65535)
@@ -496,10 +500,12 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
                        "too many members for one context (> 65535): split them over several "
                        "contexts / GPUs");
     {
-        // two short strips of ~2/5 of a big strip per member (measured 2.6 % per model
-        // step at 500x300 x 100 members against uniform strips)
+        // short strips of ~2/5 of a big strip per member, launched after every big one:
+        // two when a launch has few waves (500x300 x 100: -2.6 % per model step against
+        // uniform strips; one: +0.4 %), one when it has many (1000x600 x 1000: -0.4 %,
+        // x 125: -0.85 % against two; none: +0.5 %) -- each tail adds a strip prologue
         const int tail_rows = std::max(4, (2 * ctx->sp.by) / 5);
-        const int n_tail = ctx->sp.ny >= 4 * ctx->sp.by ? 2 : 0;
+        const int n_tail = ctx->sp.ny >= 4 * ctx->sp.by ? (stage_waves >= 6.0 ? 1 : 2) : 0;
         if (tail_rows > 0 && n_tail > 0 && tail_rows * n_tail < ctx->sp.ny && ctx->sp.ny < 32768) {
             const std::vector<int2> u = build_units(ctx->sp, tail_rows, n_tail);
             CU(DMALLOC(&ctx->units, u.size() * sizeof(int2)));
