@@ -52,10 +52,12 @@ cudaError_t dmalloc_impl(void** p, size_t bytes, const char* file, int line) {
     char* base = nullptr;
     cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&base), bytes + 2 * kGuard);
     if (e != cudaSuccess) return e;
-    // synchronous fills: the buffer is in a defined state before any stream uses it
+    // the fills run on the legacy stream, which the library's non-blocking streams do not
+    // wait for: finish them before any stream can touch the buffer
     if ((e = cudaMemset(base, kPattern, kGuard)) != cudaSuccess) return e;
     if ((e = cudaMemset(base + kGuard, 0xFF, bytes)) != cudaSuccess) return e;
     if ((e = cudaMemset(base + kGuard + bytes, kPattern, kGuard)) != cudaSuccess) return e;
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
     char* user = base + kGuard;
     std::lock_guard<std::mutex> lk(g_mu);
     registry()[user] = Alloc{bytes, file, line};

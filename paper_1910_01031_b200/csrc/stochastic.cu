@@ -153,6 +153,9 @@ using tile::kWarps;
 constexpr int kStw = TX + 4;
 static_assert(kStw * sizeof(float) % 16 == 0, "TMA box rows must be 16-byte multiples");
 
+// UNIT: scale == 1.0 (model error, posterior): scale * x == x exactly, so the three
+// products are dropped (bitwise the same)
+template <bool UNIT>
 __global__ void __launch_bounds__(tile::NT, DC_QHALF_MIN_BLOCKS)
 q_half_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrParams ep,
                     const double* __restrict__ corr, const int* __restrict__ offsets,
@@ -203,14 +206,16 @@ q_half_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrP
         const double de = S.D[rr][jl];
         const double dhu = -cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
         const double dhv = cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
-        const double e = static_cast<double>(ST[0][r][tx + 2]) + scale * de;
+        const double e = static_cast<double>(ST[0][r][tx + 2]) + (UNIT ? de : scale * de);
         if (!(heq + e > 0.0)) {
             dry = true;
             dry_at = min(dry_at, (k0 + r) * sp.nx + j);
         }
         const float fe = static_cast<float>(e);
-        const float fu = static_cast<float>(static_cast<double>(ST[1][r][tx + 2]) + scale * dhu);
-        const float fv = static_cast<float>(static_cast<double>(ST[2][r][tx + 2]) + scale * dhv);
+        const float fu = static_cast<float>(static_cast<double>(ST[1][r][tx + 2]) +
+                                            (UNIT ? dhu : scale * dhu));
+        const float fv = static_cast<float>(static_cast<double>(ST[2][r][tx + 2]) +
+                                            (UNIT ? dhv : scale * dhv));
         const size_t o = cell0 + q * step;
         eta[o] = fe;
         hu[o] = fu;
@@ -312,7 +317,11 @@ void launch_q_half_apply(cudaStream_t s, const CUtensorMap* smap, const SweParam
     // the state read and written once (24 B/cell) + the coarse field
     KScope ks(s, prof_name,
               (24.0 * sp.nx * sp.ny + 8.0 * ep.nxc * ep.nyc) * M);
-    q_half_apply_kernel<<<grid, tile::NT, 0, s>>>(*smap, sp, ep, corr, offsets, scale, eta, hu,
+    if (scale == 1.0)
+        q_half_apply_kernel<true><<<grid, tile::NT, 0, s>>>(*smap, sp, ep, corr, offsets, scale,
+                                                            eta, hu, hv, err, err_pos, mx);
+    else
+        q_half_apply_kernel<false><<<grid, tile::NT, 0, s>>>(*smap, sp, ep, corr, offsets, scale, eta, hu,
                                                   hv, err, err_pos, mx);
 }
 
