@@ -198,7 +198,7 @@ using tile::kRowsPerThread;
 using tile::kWarps;
 
 #ifndef DC_PULL_MIN_BLOCKS
-#define DC_PULL_MIN_BLOCKS 6
+#define DC_PULL_MIN_BLOCKS 5
 #endif
 
 __device__ __forceinline__ void cp_async8d(double* dst, const double* src) {
@@ -210,20 +210,34 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
 
+// The interpolation tables of one (tile, covering observation) plus everything the pull
+// derives from the window's reach, precomputed so pull_apply's loop carries no searches or
+// divisions: the column groups pass 1 evaluates, the X slots pass 2 reads, the row groups
+// and columns pass 2 evaluates, and the box the add covers.
+struct alignas(16) PullTab : tile::Tab {
+    int g0, npg;          // pass 1: column groups g0 .. g0 + npg - 1
+    int ns;               // pass 1: X slots slot[0 .. ns-1] (the ones pass 2 reads)
+    int h0, nh, ca, w;    // pass 2: row groups h0 .. h0 + nh - 1 x halo columns ca .. ca + w - 1
+    int ar0, ar1, ac0, ac1;  // the add: halo rows ar0..ar1 x halo columns ac0..ac1
+    float inv_npg, inv_w;    // 1/npg, 1/w: exact flat-index splits (index < 2^11)
+    int slot[tile::NBMAX];
+};
+constexpr int kPullTabChunks = (sizeof(PullTab) + 15) / 16;
+
 // Interpolation tables of every (tile, covering observation): they depend on the tile and
 // the observation's coarse alignment only, not on the particle, so they are built once per
 // analysis here instead of in every (particle, tile) CTA. One 96-thread CTA per entry
 // (warp 0 columns, warps 1-2 rows, as tile::setup).
 __global__ void __launch_bounds__(96)
 pull_tables_kernel(SweParams sp, ErrParams ep, const int4* __restrict__ lists,
-                   const int* __restrict__ counts, int n_obs, int tiles_x, tile::TabA* tabs) {
+                   const int* __restrict__ counts, int n_obs, int tiles_x, PullTab* tabs) {
     const int tl = blockIdx.x, li = blockIdx.y;
     if (li >= counts[tl]) return;
     const int4 ent = lists[static_cast<size_t>(tl) * n_obs + li];
     const int oj = ent.y & 0xffff, ok = ent.y >> 16, ao = ent.z, bo = ent.w;
     const int j0 = (tl % tiles_x) * TX, k0 = (tl / tiles_x) * TY;
     const int nxc = ep.nxc, nyc = ep.nyc;
-    tile::TabA& T = tabs[static_cast<size_t>(tl) * n_obs + li];
+    PullTab& T = tabs[static_cast<size_t>(tl) * n_obs + li];
     // coarse indices -> the padded window (indices 11..15 read exact zeros)
     tile::setup_cols(T, ep, sp.nx, j0, oj, [&](int a) {
         const int da = wrapf(a - ao + WH, nxc);
@@ -252,11 +266,43 @@ pull_tables_kernel(SweParams sp, ErrParams ep, const int4* __restrict__ lists,
                 T.c1 = T.cg_first[gc1 + 1] - 1;
                 T.r0 = T.rg_first[gr0];
                 T.r1 = T.rg_first[gr1 + 1] - 1;
+                // D is needed on the reach + 2 (the geostrophic differences of the cells
+                // next to it read one more D); the add covers the reach + 1
+                const int ra = max(T.r0 - 2, 0), rb = min(T.r1 + 2, tile::YH - 1);
+                const int ca = max(T.c0 - 2, 0), cb = min(T.c1 + 2, tile::XW - 1);
+                int g0 = 0, g1 = T.ncg - 1;
+                while (g0 < g1 && T.cg_first[g0 + 1] <= ca) ++g0;
+                while (g1 > g0 && T.cg_first[g1] > cb) --g1;
+                int h0 = 0, h1 = T.nrg - 1;
+                while (h0 < h1 && T.rg_first[h0 + 1] <= ra) ++h0;
+                while (h1 > h0 && T.rg_first[h1] > rb) --h1;
+                unsigned long long need = 0;
+                for (int g = h0; g <= h1; ++g)
+                    for (int q = 0; q < 4; ++q) need |= 1ull << T.rg_sl[g][q];
+                int ns = 0;
+                for (int sl = 0; sl < T.nb; ++sl)
+                    if (need >> sl & 1ull) T.slot[ns++] = sl;
+                T.g0 = g0;
+                T.npg = g1 - g0 + 1;
+                T.ns = ns;
+                T.h0 = h0;
+                T.nh = h1 - h0 + 1;
+                T.ca = ca;
+                T.w = cb - ca + 1;
+                T.ar0 = max(T.r0 - 1, 1);
+                T.ar1 = min(T.r1 + 1, TY);
+                T.ac0 = max(T.c0 - 1, 1);
+                T.ac1 = min(T.c1 + 1, TX);
+                T.inv_npg = 1.0f / static_cast<float>(T.npg);
+                T.inv_w = 1.0f / static_cast<float>(T.w);
             } else {
                 T.r0 = 1;
                 T.r1 = 0;
                 T.c0 = 1;
                 T.c1 = 0;
+                T.npg = T.ns = T.nh = T.w = 0;
+                T.ar0 = 1;
+                T.ar1 = 0;
             }
         }
     }
@@ -264,16 +310,70 @@ pull_tables_kernel(SweParams sp, ErrParams ep, const int4* __restrict__ lists,
 
 constexpr int kStw = TX + 4;  // TMA box width: cells j0-2 .. j0+TX+1 (16-byte aligned start)
 
+// i / n for i < 2^11 by a float reciprocal: (i + 0.5) * RN(1/n) stays inside
+// [q + 0.5/n, q + 1 - 0.5/n] up to a relative error of 2^-23, so truncation is exact
+__device__ __forceinline__ int div_small(int i, float inv_n) {
+    return __float2int_rz(__fmul_rn(static_cast<float>(i) + 0.5f, inv_n));
+}
+
+// pass 1 of one entry (the observation's window W through its tables T): X for the needed
+// slots x the column groups of the reach (interp_tile.cuh: one Catmull-Rom coefficient set
+// per (slot, group), the t-polynomial per fine column)
+__device__ __forceinline__ void pull_pass1(const PullTab& T, const double* __restrict__ W,
+                                           double (*X)[tile::XW]) {
+    const int n = T.ns * T.npg;
+    for (int i = threadIdx.x; i < n; i += tile::NT) {
+        const int si = div_small(i, T.inv_npg);
+        const int g = T.g0 + (i - si * T.npg);
+        const int s = T.slot[si];
+        const double* wr = W + T.brow[s];
+        const tile::Cm m = tile::coef(wr[T.cg_a[g][0]], wr[T.cg_a[g][1]], wr[T.cg_a[g][2]],
+                                      wr[T.cg_a[g][3]]);
+        const int j1 = T.cg_first[g + 1];
+        for (int jl = T.cg_first[g]; jl < j1; ++jl) X[s][jl] = tile::eval(m, T.ct[jl]);
+    }
+}
+
+// pass 2 of one entry: D on the row groups x columns of the reach + 2
+__device__ __forceinline__ void pull_pass2(const PullTab& T, const double (*X)[tile::XW],
+                                           double (*D)[tile::XW]) {
+    const int n = T.nh * T.w;
+    for (int i = threadIdx.x; i < n; i += tile::NT) {
+        const int gi = div_small(i, T.inv_w);
+        const int g = T.h0 + gi, jl = T.ca + (i - gi * T.w);
+        const tile::Cm m = tile::coef(X[T.rg_sl[g][0]][jl], X[T.rg_sl[g][1]][jl],
+                                      X[T.rg_sl[g][2]][jl], X[T.rg_sl[g][3]][jl]);
+        const int r1 = T.rg_first[g + 1];
+        for (int r = T.rg_first[g]; r < r1; ++r) D[r][jl] = tile::eval(m, T.rt[r]);
+    }
+}
+
+// Sequential-equivalent gather of every covering observation's pull into one tile of one
+// particle (optimal_proposal_pull, SPEC.md:455-463 + add_q_half, stochastic.hpp:144-160):
+// each thread keeps its cells' state in registers across all of the tile's observations
+// and adds them in ascending id, rounding to float after every add as the reference's
+// per-observation add_q_half does. The observations run as a two-barrier software
+// pipeline: while entry i is added from its D, entry i+1's pass 1 fills X; then entry
+// i+1's pass 2 fills the other D while entry i+2's window and tables stream in.
+struct PullSmem {
+    union alignas(128) {  // the TMA box of the tile's state (128-byte aligned), then (once
+        float ST[3][TY][kStw];  // in registers) the second D
+        double D1[tile::YH][tile::XW];
+    } u;
+    double W[2][WP * WP];
+    PullTab T[2];
+    double X[tile::NBMAX][tile::XW];
+    double D0[tile::YH][tile::XW];
+    unsigned long long bar;
+};
+
 __global__ void __launch_bounds__(tile::NT, DC_PULL_MIN_BLOCKS)
 pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrParams ep,
                   const double* __restrict__ win, int n_obs,
                   const int4* __restrict__ lists, const int* __restrict__ counts, int tiles_x,
-                  const tile::TabA* __restrict__ tabs, float* eta, float* hu, float* hv,
+                  const PullTab* __restrict__ tabs, float* eta, float* hu, float* hv,
                   int* err, int* err_pos) {
-    __shared__ double W[WP * WP];
-    __shared__ tile::Smem S;
-    __shared__ alignas(128) float ST[3][TY][kStw];  // the tile's state across all observations
-    __shared__ alignas(8) unsigned long long bar;
+    __shared__ alignas(128) PullSmem P;
     const int m = blockIdx.y;
     // another tile of the member may raise E_DRY_ADD meanwhile: decide once per CTA
     if (__syncthreads_or(err[m] != 0)) return;
@@ -283,99 +383,99 @@ pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrPar
     const int j0 = (tl % tiles_x) * TX, k0 = (tl / tiles_x) * TY;
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
     const int j = j0 + tx;
-    const size_t mbase = static_cast<size_t>(m) * sp.mstride;
-    // the tile's state arrives in shared memory by one TMA box (cells j0-2 .. j0+TX+1, TY
-    // rows, 3 fields) and stays there across all the tile's observations; each thread then
-    // owns its cells, so the fold needs no further barrier for them
-    const uint32_t b = smem_u32(&bar);
+    const uint32_t b = smem_u32(&P.bar);
     if (tid == 0) {
         mbar_init(b, 1);
         mbar_fence_init();
-        mbar_expect_tx(b, sizeof(ST));
-        tma_row(smem_u32(&ST[0][0][0]), &smap, j0, m * (sp.ny + 4) + 2 + k0, b);
+        mbar_expect_tx(b, sizeof(P.u.ST));
+        tma_row(smem_u32(&P.u.ST[0][0][0]), &smap, j0, m * (sp.ny + 4) + 2 + k0, b);
     }
-    // the window pad stays zero: the copies below touch only da, db < WIN
-    for (int i = tid; i < WP * WP; i += tile::NT) W[i] = 0.0;
-    __syncthreads();
+    // the windows' pad (da or db >= WIN) stays zero; the copies touch only da, db < WIN
+    for (int i = tid; i < 2 * WP * WP; i += tile::NT) {
+        const int e = i & (WP * WP - 1);
+        if ((e & (WP - 1)) >= WIN || (e >> 4) >= WIN) P.W[i >> 8][e] = 0.0;
+    }
     const int4* tlist = lists + static_cast<size_t>(tl) * n_obs;
-    const tile::TabA* ttab = tabs + static_cast<size_t>(tl) * n_obs;
+    const PullTab* ttab = tabs + static_cast<size_t>(tl) * n_obs;
     const double* wbase = win + static_cast<size_t>(m) * n_obs * (WIN * WIN);
-    auto load_win = [&](int li) {  // observation li's 11x11 window into the padded 16x16
+    auto load = [&](int li) {  // entry li's 11x11 window and tables into buffer li & 1
+        const int q = li & 1;
         if (tid < WIN * WIN)
-            cp_async8d(&W[(tid / WIN) * WP + tid % WIN],
+            cp_async8d(&P.W[q][(tid / WIN) * WP + tid % WIN],
                        wbase + static_cast<size_t>(tlist[li].x) * (WIN * WIN) + tid);
+        for (int c = tid; c < kPullTabChunks; c += tile::NT)
+            cp_async16(reinterpret_cast<char*>(&P.T[q]) + 16 * c,
+                       reinterpret_cast<const char*>(ttab + li) + 16 * c);
+        asm volatile("cp.async.commit_group;\n" ::);
     };
-    auto load_tab = [&](int li) {
-        if (tid < tile::kTabChunks)
-            cp_async16(reinterpret_cast<char*>(&S.t) + 16 * tid,
-                       reinterpret_cast<const char*>(ttab + li) + 16 * tid);
-    };
-    load_win(0);
-    load_tab(0);
-    asm volatile("cp.async.commit_group;\n" ::);
+    load(0);
+    if (cnt > 1) load(1);
+    // the thread's cells: halo row ty + 1 + kWarps q, halo column tx + 1
+    float se[kRowsPerThread], su[kRowsPerThread], sv[kRowsPerThread];
+    __syncthreads();  // the mbarrier is initialised
+    mbar_wait(b, 0);
+#pragma unroll
+    for (int q = 0; q < kRowsPerThread; ++q) {
+        const int r = min(ty + kWarps * q, TY - 1);
+        se[q] = P.u.ST[0][r][tx + 2];
+        su[q] = P.u.ST[1][r][tx + 2];
+        sv[q] = P.u.ST[2][r][tx + 2];
+    }
+    if (cnt > 1) asm volatile("cp.async.wait_group 1;\n" ::);
+    else asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();  // entry 0 landed; the state box is in registers (D1 may be written)
+    if (P.T[0].ns > 0) pull_pass1(P.T[0], P.W[0], P.X);
+    __syncthreads();
+    if (P.T[0].nh > 0) pull_pass2(P.T[0], P.X, P.D0);
     bool dry = false;
     int dry_at = 0x7fffffff;
     const double cy = ep.cy, cx = ep.cx, heq = ep.h_eq;
-    mbar_wait(b, 0);  // the tile state
+    const bool colok = j < sp.nx;
     for (int li = 0; li < cnt; ++li) {
-        // entry li's window and tables have landed
         asm volatile("cp.async.wait_group 0;\n" ::);
-        __syncthreads();
+        __syncthreads();  // D of entry li complete, X free, entry li+1 landed
         const bool more = li + 1 < cnt;
-        // the window's reach in this tile (halo coordinates); outside it the pull is an
-        // exact zero, whose add leaves the float state unchanged
-        const int r0 = S.t.r0, r1 = S.t.r1, c0 = S.t.c0, c1 = S.t.c1;
-        if (r0 > r1) {  // out of reach: nothing to add; prefetch the next entry
-            __syncthreads();  // every thread has read the box before the tables are reused
-            if (more) {
-                load_win(li + 1);
-                load_tab(li + 1);
-            }
-            asm volatile("cp.async.commit_group;\n" ::);
-            continue;
-        }
-        // D on the reach + 2 (the geostrophic differences of the cells next to it read one
-        // more D), applied on the reach + 1
-        tile::interpolate_box(
-            S, max(r0 - 2, 0), min(r1 + 2, tile::YH - 1), max(c0 - 2, 0),
-            min(c1 + 2, tile::XW - 1), [&](int brow, int a) { return W[brow + a]; },
-            [&] {  // pass 1 done: the window is free, fetch the next observation's
-                if (more) load_win(li + 1);
-            },
-            [&] {  // pass 2 done: the tables are free
-                if (more) load_tab(li + 1);
-                asm volatile("cp.async.commit_group;\n" ::);
-            });
-        const int ar0 = max(r0 - 1, 1), ar1 = min(r1 + 1, TY);
-        const int ac0 = max(c0 - 1, 1), ac1 = min(c1 + 1, TX);
-        const bool colin = tx + 1 >= ac0 && tx + 1 <= ac1;
+        const PullTab& Tn = P.T[(li + 1) & 1];
+        if (more && Tn.ns > 0) pull_pass1(Tn, P.W[(li + 1) & 1], P.X);
+        // entry li's add on its box (outside it the pull is an exact zero, whose add leaves
+        // the float state unchanged)
+        {
+            const PullTab& T = P.T[li & 1];
+            const double(*D)[tile::XW] = (li & 1) ? P.u.D1 : P.D0;
+            const int ar0 = T.ar0, ar1 = T.ar1;
+            const int jl = tx + 1;
+            const bool colin = colok && jl >= T.ac0 && jl <= T.ac1;
 #pragma unroll
-        for (int q = 0; q < kRowsPerThread; ++q) {
-            const int r = ty + kWarps * q, k = k0 + r;
-            if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
-            const int rr = r + 1, jl = tx + 1;
-            if (!colin || rr < ar0 || rr > ar1) continue;
-            const double de = S.D[rr][jl];
-            const double dhu = -cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
-            const double dhv = cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
-            const double ee = static_cast<double>(ST[0][r][tx + 2]) + 1.0 * de;
-            if (!(heq + ee > 0.0)) {
-                dry = true;
-                dry_at = min(dry_at, k * sp.nx + j);
+            for (int q = 0; q < kRowsPerThread; ++q) {
+                const int r = ty + kWarps * q, rr = r + 1, k = k0 + r;
+                if (r >= TY || rr < ar0 || rr > ar1) continue;  // warp-uniform
+                if (!colin || k >= sp.ny) continue;
+                const double de = D[rr][jl];
+                const double dhu = -cy * (D[rr + 1][jl] - D[rr - 1][jl]);
+                const double dhv = cx * (D[rr][jl + 1] - D[rr][jl - 1]);
+                const double ee = static_cast<double>(se[q]) + 1.0 * de;
+                if (!(heq + ee > 0.0)) {
+                    dry = true;
+                    dry_at = min(dry_at, k * sp.nx + j);
+                }
+                se[q] = static_cast<float>(ee);
+                su[q] = static_cast<float>(static_cast<double>(su[q]) + 1.0 * dhu);
+                sv[q] = static_cast<float>(static_cast<double>(sv[q]) + 1.0 * dhv);
             }
-            ST[0][r][tx + 2] = static_cast<float>(ee);
-            ST[1][r][tx + 2] = static_cast<float>(static_cast<double>(ST[1][r][tx + 2]) + 1.0 * dhu);
-            ST[2][r][tx + 2] = static_cast<float>(static_cast<double>(ST[2][r][tx + 2]) + 1.0 * dhv);
         }
+        __syncthreads();  // X complete; entry li's window, tables and D are free
+        if (li + 2 < cnt) load(li + 2);
+        if (more && Tn.nh > 0) pull_pass2(Tn, P.X, (li & 1) ? P.D0 : P.u.D1);
     }
+    const size_t mbase = static_cast<size_t>(m) * sp.mstride;
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
         const int r = ty + kWarps * q, k = k0 + r;
-        if (r >= TY || k >= sp.ny || j >= sp.nx) continue;
+        if (r >= TY || k >= sp.ny || !colok) continue;
         const size_t o = mbase + static_cast<size_t>(k) * sp.pitch + j;
-        eta[o] = ST[0][r][tx + 2];
-        hu[o] = ST[1][r][tx + 2];
-        hv[o] = ST[2][r][tx + 2];
+        eta[o] = se[q];
+        hu[o] = su[q];
+        hv[o] = sv[q];
     }
     if (dry) {
         atomicCAS(err + m, 0, E_DRY_ADD);
@@ -717,23 +817,23 @@ void launch_tile_lists(cudaStream_t s, const SweParams& sp, const ErrParams& ep,
     *tiles_x_out = tiles_x;
 }
 
-size_t pull_table_bytes() { return sizeof(tile::TabA); }
+size_t pull_table_bytes() { return sizeof(PullTab); }
 
 void launch_pull_apply(cudaStream_t s, const CUtensorMap* smap, const SweParams& sp,
                        const ErrParams& ep, const double* win,
                        const int* cells, int n_obs, const int* lists, const int* counts,
                        int n_tiles, int tiles_x, void* tabs, float* eta, float* hu, float* hv,
                        int* err, int* err_pos, int M, double entries, double touched_cells) {
-    tile::TabA* T = static_cast<tile::TabA*>(tabs);
+    PullTab* T = static_cast<PullTab*>(tabs);
     {
-        KScope ks(s, "pull_tables", entries * (sizeof(tile::TabA) + 16.0));
+        KScope ks(s, "pull_tables", entries * (sizeof(PullTab) + 16.0));
         pull_tables_kernel<<<dim3(n_tiles, n_obs), 96, 0, s>>>(
             sp, ep, reinterpret_cast<const int4*>(lists), counts, n_obs, tiles_x, T);
     }
     // the touched tiles' state read and written once (24 B/cell), every (member, obs)
     // window once, the tables once
     KScope ks(s, "pull_apply", (24.0 * touched_cells + 8.0 * WIN * WIN * n_obs) * M +
-                                   entries * sizeof(tile::TabA));
+                                   entries * sizeof(PullTab));
     pull_apply_kernel<<<dim3(n_tiles, M), tile::NT, 0, s>>>(*smap, sp, ep, win, n_obs,
                                                        reinterpret_cast<const int4*>(lists), counts,
                                                        tiles_x, T, eta, hu, hv, err, err_pos);
