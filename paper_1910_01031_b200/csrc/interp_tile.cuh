@@ -48,15 +48,6 @@ struct Tab {
     // when the tile is outside the window's reach
     int r0, r1, c0, c1;
 };
-struct alignas(16) TabA : Tab {};  // 16-byte aligned, copied with 16-byte cp.async
-constexpr int kTabChunks = (sizeof(TabA) + 15) / 16;
-
-struct Smem {
-    double X[NBMAX][XW];
-    double D[YH][XW];
-    TabA t;
-};
-
 struct Cm {
     double a, b, c, d;
 };
@@ -89,8 +80,8 @@ __device__ __forceinline__ unsigned lanemask_le() {
 
 // Column tables of one tile (warp 0): depend only on the tile's columns and the coarse
 // column offset, so a CTA that streams down a column strip builds them once. No barrier.
-template <class COLMAP>
-__device__ __forceinline__ void setup_cols(Tab& S, const ErrParams& ep, int nx, int j0, int oj,
+template <class TabT, class COLMAP>
+__device__ __forceinline__ void setup_cols(TabT& S, const ErrParams& ep, int nx, int j0, int oj,
                                            COLMAP colmap) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) {  // columns l and 32+l (l < 2) (stochastic.hpp:104-108)
@@ -177,93 +168,6 @@ __device__ __forceinline__ void setup_rows(Tab& S, const ErrParams& ep, int ny, 
             if (lane == 0) S.nb = nb;
         }
     }
-}
-
-// Tables for one (tile, coarse offset): COLMAP / ROWMAP turn wrapped coarse indices into
-// whatever the value accessor expects. Warp 0 builds the column groups, warp 1 the row
-// groups (one lane per halo row), warp 2 the X-slot rows. Ends with a barrier.
-template <class COLMAP, class ROWMAP>
-__device__ __forceinline__ void setup(Smem& S, const ErrParams& ep, int nx, int ny, int j0,
-                                      int k0, int oj, int ok, COLMAP colmap, ROWMAP rowmap) {
-    setup_cols(S.t, ep, nx, j0, oj, colmap);
-    setup_rows(S.t, ep, ny, k0, ok, rowmap);
-    __syncthreads();
-}
-
-struct NoHook {
-    __device__ __forceinline__ void operator()() const {}
-};
-
-// Passes 1 and 2 restricted to a box (pull_apply): X for the column groups meeting halo
-// columns [ca, cb], D for the row groups meeting halo rows [ra, rb] and columns [ca, cb].
-// Outside the observation's reach the interpolated field is exactly zero, so a caller that
-// needs D on a box around the reach computes exactly the values the full passes would.
-template <class VALF, class H1 = NoHook, class H2 = NoHook>
-__device__ __forceinline__ void interpolate_box(Smem& S, int ra, int rb, int ca, int cb,
-                                                VALF valf, H1 after1 = H1{},
-                                                H2 after2 = H2{}) {
-    const Tab& T = S.t;
-    const int tid = threadIdx.x;
-    // column groups meeting [ca, cb]: g0 .. g1
-    int g0 = 0, g1 = T.ncg - 1;
-    while (g0 < g1 && T.cg_first[g0 + 1] <= ca) ++g0;
-    while (g1 > g0 && T.cg_first[g1] > cb) --g1;
-    const int ncg = g1 - g0 + 1, n1 = T.nb * ncg;
-    for (int i = tid; i < n1; i += NT) {  // (X slot, column group)
-        const int s = i / ncg, g = g0 + (i - s * ncg);
-        const int b = T.brow[s];
-        const Cm m = coef(valf(b, T.cg_a[g][0]), valf(b, T.cg_a[g][1]), valf(b, T.cg_a[g][2]),
-                          valf(b, T.cg_a[g][3]));
-        const int j1 = T.cg_first[g + 1];
-        for (int jl = T.cg_first[g]; jl < j1; ++jl) S.X[s][jl] = eval(m, T.ct[jl]);
-    }
-    __syncthreads();
-    after1();
-    int h0 = 0, h1 = T.nrg - 1;
-    while (h0 < h1 && T.rg_first[h0 + 1] <= ra) ++h0;
-    while (h1 > h0 && T.rg_first[h1] > rb) --h1;
-    const int w = cb - ca + 1, n2 = (h1 - h0 + 1) * w;
-    for (int i = tid; i < n2; i += NT) {  // (row group, halo column)
-        const int g = h0 + i / w, jl = ca + (i - (g - h0) * w);
-        const Cm m = coef(S.X[T.rg_sl[g][0]][jl], S.X[T.rg_sl[g][1]][jl], S.X[T.rg_sl[g][2]][jl],
-                          S.X[T.rg_sl[g][3]][jl]);
-        const int r1 = T.rg_first[g + 1];
-        for (int r = T.rg_first[g]; r < r1; ++r) S.D[r][jl] = eval(m, T.rt[r]);
-    }
-    __syncthreads();
-    after2();
-}
-
-// Passes 1 and 2 into S.D from the tables in S.t. VALF(mapped row, mapped col) returns the
-// coarse value. Ends with a barrier. after1 runs right after the barrier that ends pass 1
-// (the coarse values are no longer read), after2 after the final barrier (the tables are
-// no longer read) -- where pull_apply prefetches the next observation's window / tables.
-template <class VALF, class H1 = NoHook, class H2 = NoHook>
-__device__ __forceinline__ void interpolate(Smem& S, VALF valf, H1 after1 = H1{},
-                                            H2 after2 = H2{}) {
-    const Tab& T = S.t;
-    const int tid = threadIdx.x;
-    const int ncg = T.ncg, n1 = T.nb * ncg;
-    for (int i = tid; i < n1; i += NT) {  // (X slot, column group)
-        const int s = i / ncg, g = i - s * ncg;
-        const int b = T.brow[s];
-        const Cm m = coef(valf(b, T.cg_a[g][0]), valf(b, T.cg_a[g][1]), valf(b, T.cg_a[g][2]),
-                          valf(b, T.cg_a[g][3]));
-        const int j1 = T.cg_first[g + 1];
-        for (int jl = T.cg_first[g]; jl < j1; ++jl) S.X[s][jl] = eval(m, T.ct[jl]);
-    }
-    __syncthreads();
-    after1();
-    const int n2 = T.nrg * XW;
-    for (int i = tid; i < n2; i += NT) {  // (row group, halo column)
-        const int g = i / XW, jl = i - g * XW;
-        const Cm m = coef(S.X[T.rg_sl[g][0]][jl], S.X[T.rg_sl[g][1]][jl], S.X[T.rg_sl[g][2]][jl],
-                          S.X[T.rg_sl[g][3]][jl]);
-        const int r1 = T.rg_first[g + 1];
-        for (int r = T.rg_first[g]; r < r1; ++r) S.D[r][jl] = eval(m, T.rt[r]);
-    }
-    __syncthreads();
-    after2();
 }
 
 } // namespace tile

@@ -143,8 +143,11 @@ __device__ __forceinline__ unsigned ordered_bits(float f) {
 // swe.hpp:306-317) so the next model step needs no separate scan.
 using tile::kRowsPerThread;
 using tile::kWarps;
+#ifndef DC_QHALF_WAVES
+#define DC_QHALF_WAVES 8.0
+#endif
 #ifndef DC_QHALF_MIN_BLOCKS
-#define DC_QHALF_MIN_BLOCKS 6
+#define DC_QHALF_MIN_BLOCKS 5
 #endif
 
 // The tile's state arrives by TMA: one box {TX+4 columns from cell j0-2, TY rows, 3 fields}
@@ -153,6 +156,100 @@ using tile::kWarps;
 constexpr int kStw = TX + 4;
 static_assert(kStw * sizeof(float) % 16 == 0, "TMA box rows must be 16-byte multiples");
 
+// Strip form: one CTA streams down a column strip of S tiles of one member (32 columns x
+// S*30 rows). The column tables are built once per strip; the x pass (X, one row per
+// coarse row) lives in a ring keyed by the coarse row's unwrapped index, so a coarse row
+// shared by consecutive tiles is evaluated once; the tiles run as a two-barrier software
+// pipeline -- the add of tile i beside the x pass of tile i+1's new coarse rows, then the
+// y pass of tile i+1 into the other D while tile i+1's state arrives by TMA.
+struct QhCols {  // column tables of the strip (interp_tile.cuh setup_cols, identity map)
+    double ct[tile::XW];
+    int cg_a[tile::XW][4];
+    int cg_first[tile::XW + 1];
+    int ncg;
+};
+struct QhRows {  // row tables of one tile: one lane of warp 1 per halo row
+    double rt[tile::YH];
+    int rg_first[tile::YH + 1];
+    int rg_u[tile::YH];  // unwrapped coarse row b0 of each row group
+    int rg_slot[tile::YH][4];  // ring slots of its four coarse rows b0-1 .. b0+2
+    int nrg, u_last;     // u_last: the last coarse row the tile reads (b0 of row 31, + 2)
+};
+struct QhSmem {
+    float ST[3][TY][kStw];       // the tile's state box (TMA), 128-byte aligned at offset 0
+    double D[2][tile::YH][tile::XW];
+    QhCols C;
+    QhRows R[2];
+    float red[3][kWarps];
+    unsigned long long bar;
+    // then X[ring][XW] doubles (dynamic)
+};
+__host__ __device__ constexpr int qh_ring(int c) { return 31 / c + 6; }
+
+__device__ __forceinline__ int qh_slot(int u, int ring) { return (u + 4 * ring) % ring; }
+
+// halo rows of the tile starting at fine row k0 (warp 1, lane = halo row): b0 and t as
+// interpolate_bicubic computes them (stochastic.hpp:98-102) from the wrapped row, and the
+// unwrapped coarse index u = b0 -/+ nyc for halo rows above / below the domain
+__device__ __forceinline__ void qh_rows(QhRows& R, const ErrParams& ep, int ny, int k0, int ok,
+                                        int ring) {
+    const int lane = threadIdx.x & 31;
+    const int k = k0 - 1 + lane;
+    int b0;
+    double t;
+    tile::row_b0(ep, wrap1(k, ny), ok, &b0, &t);
+    const int u = b0 + (k < 0 ? -ep.nyc : (k >= ny ? ep.nyc : 0));
+    const int up = __shfl_up_sync(0xffffffffu, u, 1);
+    const bool st = lane == 0 || u != up;
+    const unsigned bl = __ballot_sync(0xffffffffu, st);
+    R.rt[lane] = t;
+    if (st) {
+        const int g = __popc(bl & tile::lanemask_le()) - 1;
+        R.rg_first[g] = lane;
+        R.rg_u[g] = u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) R.rg_slot[g][q] = qh_slot(u - 1 + q, ring);
+    }
+    if (lane == 31) {
+        const int n = __popc(bl);
+        R.nrg = n;
+        R.rg_first[n] = tile::YH;
+        R.u_last = u + 2;
+    }
+}
+
+// x pass of coarse rows u0 .. u1 (unwrapped) into their ring slots
+__device__ __forceinline__ void qh_xpass(const QhCols& C, const ErrParams& ep,
+                                         const double* __restrict__ cf, double (*X)[tile::XW],
+                                         int ring, int u0, int u1) {
+    const int ncg = C.ncg, n = (u1 - u0 + 1) * ncg;
+    const float inv_ncg = 1.0f / static_cast<float>(ncg);
+    for (int i = threadIdx.x; i < n; i += tile::NT) {
+        const int ui = __float2int_rz(__fmul_rn(static_cast<float>(i) + 0.5f, inv_ncg));
+        const int g = i - ui * ncg;
+        const int u = u0 + ui;
+        const double* row = cf + det::wrapf(u, ep.nyc) * ep.nxc;
+        const tile::Cm m = tile::coef(__ldg(row + C.cg_a[g][0]), __ldg(row + C.cg_a[g][1]),
+                                      __ldg(row + C.cg_a[g][2]), __ldg(row + C.cg_a[g][3]));
+        double* x = X[qh_slot(u, ring)];
+        const int j1 = C.cg_first[g + 1];
+        for (int jl = C.cg_first[g]; jl < j1; ++jl) x[jl] = tile::eval(m, C.ct[jl]);
+    }
+}
+
+// y pass of one tile: D on all 32 halo rows x 34 halo columns
+__device__ __forceinline__ void qh_ypass(const QhRows& R, const double (*X)[tile::XW],
+                                         double (*D)[tile::XW]) {
+    const int n = R.nrg * tile::XW;
+    for (int i = threadIdx.x; i < n; i += tile::NT) {
+        const int g = i / tile::XW, jl = i - g * tile::XW;
+        const tile::Cm m = tile::coef(X[R.rg_slot[g][0]][jl], X[R.rg_slot[g][1]][jl],
+                                      X[R.rg_slot[g][2]][jl], X[R.rg_slot[g][3]][jl]);
+        const int r1 = R.rg_first[g + 1];
+        for (int r = R.rg_first[g]; r < r1; ++r) D[r][jl] = tile::eval(m, R.rt[r]);
+    }
+}
+
 // UNIT: scale == 1.0 (model error, posterior): scale * x == x exactly, so the three
 // products are dropped (bitwise the same)
 template <bool UNIT>
@@ -160,94 +257,115 @@ __global__ void __launch_bounds__(tile::NT, DC_QHALF_MIN_BLOCKS)
 q_half_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrParams ep,
                     const double* __restrict__ corr, const int* __restrict__ offsets,
                     double scale, float* eta, float* hu, float* hv, int* err, int* err_pos,
-                    unsigned* mx) {
-    __shared__ tile::Smem S;
-    __shared__ alignas(128) float ST[3][TY][kStw];
-    __shared__ float red[3][kWarps];
-    __shared__ alignas(8) unsigned long long bar;
+                    unsigned* mx, int strip_tiles) {
+    extern __shared__ __align__(128) unsigned char qh_raw[];
+    QhSmem& S = *reinterpret_cast<QhSmem*>(qh_raw);
+    double(*X)[tile::XW] = reinterpret_cast<double(*)[tile::XW]>(qh_raw + sizeof(QhSmem));
     const int m = blockIdx.z;
     // another tile of the member may raise E_DRY_ADD meanwhile: decide once per CTA
     if (__syncthreads_or(err[m] != 0)) return;
-    const int j0 = blockIdx.x * TX, k0 = blockIdx.y * TY;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int n_tiles_y = (sp.ny + TY - 1) / TY;
+    const int t0 = blockIdx.y * strip_tiles, nt = min(strip_tiles, n_tiles_y - t0);
+    const int j0 = blockIdx.x * TX;
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5, warp = ty;
     const int j = j0 + tx;
+    const int ring = qh_ring(ep.c);
     const size_t pitch = sp.pitch;
-    // this thread's cells: column j, rows k0 + ty + 8q
-    const size_t cell0 = static_cast<size_t>(m) * sp.mstride + static_cast<size_t>(k0 + ty) * pitch + j;
-    const size_t step = static_cast<size_t>(kWarps) * pitch;
-    const uint32_t b = smem_u32(&bar);
-    if (threadIdx.x == 0) {
-        mbar_init(b, 1);
-        mbar_fence_init();
-        mbar_expect_tx(b, sizeof(ST));
-        // storage row of cell row k0 of member m (the map starts at row -2 of member 0)
-        tma_row(smem_u32(&ST[0][0][0]), &smap, j0, m * (sp.ny + 4) + 2 + k0, b);
-    }
     const int oj = offsets[2 * m], ok = offsets[2 * m + 1];
     const double* cf = corr + static_cast<size_t>(m) * ep.nxc * ep.nyc;
-    const int nxc = ep.nxc;
-    tile::setup(S, ep, sp.nx, sp.ny, j0, k0, oj, ok, [](int a) { return a; },
-                [&](int bb) { return bb * nxc; });  // (its barrier publishes the mbarrier)
-    tile::interpolate(S, [&](int brow, int a) { return __ldg(cf + brow + a); });
-    // geostrophic balance (stochastic.hpp:122-139) + add in fp64, cast to float
+    // the member's fields (a member's storage is < 2^31 cells: 32-bit offsets below)
+    float* const Em = eta + static_cast<size_t>(m) * sp.mstride;
+    float* const Um = hu + static_cast<size_t>(m) * sp.mstride;
+    float* const Vm = hv + static_cast<size_t>(m) * sp.mstride;
+    const uint32_t b = smem_u32(&S.bar);
+    if (tid == 0) {
+        mbar_init(b, 1);
+        mbar_fence_init();
+        mbar_expect_tx(b, sizeof(S.ST));
+        // storage row of cell row k0 of member m (the map starts at row -2 of member 0)
+        tma_row(smem_u32(&S.ST[0][0][0]), &smap, j0, m * (sp.ny + 4) + 2 + t0 * TY, b);
+    }
+    tile::setup_cols(S.C, ep, sp.nx, j0, oj, [](int a) { return a; });
+    if (warp == 1) qh_rows(S.R[0], ep, sp.ny, t0 * TY, ok, ring);
+    __syncthreads();
+    qh_xpass(S.C, ep, cf, X, ring, S.R[0].rg_u[0] - 1, S.R[0].u_last);
+    if (warp == 1 && nt > 1) qh_rows(S.R[1], ep, sp.ny, (t0 + 1) * TY, ok, ring);
+    __syncthreads();
+    qh_ypass(S.R[0], X, S.D[0]);
     bool dry = false;
     int dry_at = 0x7fffffff;
     float mx_u = 0.0f, mx_v = 0.0f, mn_h = 3.402823466e+38f;
     const double cy = ep.cy, cx = ep.cx, heq = ep.h_eq;
-    mbar_wait(b, 0);
-    // cells within 2 of a domain edge also go to their ghost copies, so the
-    // next model step needs no fix_ghosts pass; interior tiles skip that (uniform branch)
-    const bool edge = j0 < 2 || j0 + TX > sp.nx - 2 || k0 < 2 || k0 + TY > sp.ny - 2;
+    for (int i = 0; i < nt; ++i) {
+        __syncthreads();  // D of tile i complete; tile i+1's row tables published
+        const int k0 = (t0 + i) * TY;
+        if (i + 1 < nt) qh_xpass(S.C, ep, cf, X, ring, S.R[i & 1].u_last + 1, S.R[(i + 1) & 1].u_last);
+        // geostrophic balance (stochastic.hpp:122-139) + add in fp64, cast to float
+        mbar_wait(b, i & 1);
+        const double(*D)[tile::XW] = S.D[i & 1];
+        // cells within 2 of a domain edge also go to their ghost copies, so
+        // the next model step needs no fix_ghosts pass; interior tiles skip that (uniform)
+        const bool edge = j0 < 2 || j0 + TX > sp.nx - 2 || k0 < 2 || k0 + TY > sp.ny - 2;
+        const int cell0 = (k0 + ty) * static_cast<int>(pitch) + j;  // offset in the member
 #pragma unroll
-    for (int q = 0; q < kRowsPerThread; ++q) {
-        const int r = ty + kWarps * q;
-        if (!((r < TY) && (k0 + r < sp.ny) && (j < sp.nx))) continue;
-        const int rr = r + 1, jl = tx + 1;
-        const double de = S.D[rr][jl];
-        const double dhu = -cy * (S.D[rr + 1][jl] - S.D[rr - 1][jl]);
-        const double dhv = cx * (S.D[rr][jl + 1] - S.D[rr][jl - 1]);
-        const double e = static_cast<double>(ST[0][r][tx + 2]) + (UNIT ? de : scale * de);
-        if (!(heq + e > 0.0)) {
-            dry = true;
-            dry_at = min(dry_at, (k0 + r) * sp.nx + j);
-        }
-        const float fe = static_cast<float>(e);
-        const float fu = static_cast<float>(static_cast<double>(ST[1][r][tx + 2]) +
-                                            (UNIT ? dhu : scale * dhu));
-        const float fv = static_cast<float>(static_cast<double>(ST[2][r][tx + 2]) +
-                                            (UNIT ? dhv : scale * dhv));
-        const size_t o = cell0 + q * step;
-        eta[o] = fe;
-        hu[o] = fu;
-        hv[o] = fv;
-        if (edge) {
-            const int kk = k0 + r;
-            const ptrdiff_t gc = j < 2 ? sp.nx : (j >= sp.nx - 2 ? -sp.nx : 0);
-            const ptrdiff_t gr = kk < 2 ? sp.ny : (kk >= sp.ny - 2 ? -sp.ny : 0);
-            if (gc) {
-                eta[o + gc] = fe;
-                hu[o + gc] = fu;
-                hv[o + gc] = fv;
+        for (int q = 0; q < kRowsPerThread; ++q) {
+            const int r = ty + kWarps * q;
+            if (!((r < TY) && (k0 + r < sp.ny) && (j < sp.nx))) continue;
+            const int rr = r + 1, jl = tx + 1;
+            const double de = D[rr][jl];
+            const double dhu = -cy * (D[rr + 1][jl] - D[rr - 1][jl]);
+            const double dhv = cx * (D[rr][jl + 1] - D[rr][jl - 1]);
+            const float s0 = S.ST[0][r][tx + 2], s1 = S.ST[1][r][tx + 2], s2 = S.ST[2][r][tx + 2];
+            const double e = static_cast<double>(s0) + (UNIT ? de : scale * de);
+            if (!(heq + e > 0.0)) {
+                dry = true;
+                dry_at = min(dry_at, (k0 + r) * sp.nx + j);
             }
-            if (gr) {
-                const ptrdiff_t g = gr * static_cast<ptrdiff_t>(pitch);
-                eta[o + g] = fe;
-                hu[o + g] = fu;
-                hv[o + g] = fv;
+            const float fe = static_cast<float>(e);
+            const float fu = static_cast<float>(static_cast<double>(s1) + (UNIT ? dhu : scale * dhu));
+            const float fv = static_cast<float>(static_cast<double>(s2) + (UNIT ? dhv : scale * dhv));
+            const int o = cell0 + q * kWarps * static_cast<int>(pitch);
+            Em[o] = fe;
+            Um[o] = fu;
+            Vm[o] = fv;
+            if (edge) {
+                const int kk = k0 + r;
+                const int gc = j < 2 ? sp.nx : (j >= sp.nx - 2 ? -sp.nx : 0);
+                const int gr = kk < 2 ? sp.ny : (kk >= sp.ny - 2 ? -sp.ny : 0);
                 if (gc) {
-                    eta[o + g + gc] = fe;
-                    hu[o + g + gc] = fu;
-                    hv[o + g + gc] = fv;
+                    Em[o + gc] = fe;
+                    Um[o + gc] = fu;
+                    Vm[o + gc] = fv;
+                }
+                if (gr) {
+                    const int g = gr * static_cast<int>(pitch);
+                    Em[o + g] = fe;
+                    Um[o + g] = fu;
+                    Vm[o + g] = fv;
+                    if (gc) {
+                        Em[o + g + gc] = fe;
+                        Um[o + g + gc] = fu;
+                        Vm[o + g + gc] = fv;
+                    }
                 }
             }
+            if (mx) {  // load() statistics of the new state, IEEE float (swe.hpp:307-316)
+                const float h = __fadd_rn(sp.H, fe);
+                mn_h = fminf(mn_h, h);
+                const float inv = rcp_rn(h);
+                const float c = sqrt_rn(__fmul_rn(sp.g, fmaxf(h, 0.0f)));
+                mx_u = fmaxf(mx_u, __fadd_rn(fabsf(__fmul_rn(fu, inv)), c));
+                mx_v = fmaxf(mx_v, __fadd_rn(fabsf(__fmul_rn(fv, inv)), c));
+            }
         }
-        if (mx) {  // load() statistics of the new state, IEEE float (swe.hpp:307-316)
-            const float h = __fadd_rn(sp.H, fe);
-            mn_h = fminf(mn_h, h);
-            const float inv = rcp_rn(h);
-            const float c = sqrt_rn(__fmul_rn(sp.g, fmaxf(h, 0.0f)));
-            mx_u = fmaxf(mx_u, __fadd_rn(fabsf(__fmul_rn(fu, inv)), c));
-            mx_v = fmaxf(mx_v, __fadd_rn(fabsf(__fmul_rn(fv, inv)), c));
+        __syncthreads();  // the state box is consumed; tile i+1's new X rows are complete
+        if (i + 1 < nt) {
+            if (tid == 0) {
+                mbar_expect_tx(b, sizeof(S.ST));
+                tma_row(smem_u32(&S.ST[0][0][0]), &smap, j0, m * (sp.ny + 4) + 2 + k0 + TY, b);
+            }
+            if (warp == 1 && i + 2 < nt) qh_rows(S.R[i & 1], ep, sp.ny, k0 + 2 * TY, ok, ring);
+            qh_ypass(S.R[(i + 1) & 1], X, S.D[(i + 1) & 1]);
         }
     }
     if (dry) {
@@ -261,17 +379,17 @@ q_half_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrP
         asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(b_) : "f"(mx_v));
         asm("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(c_) : "f"(mn_h));
         if (tx == 0) {
-            red[0][ty] = a_;
-            red[1][ty] = b_;
-            red[2][ty] = c_;
+            S.red[0][ty] = a_;
+            S.red[1][ty] = b_;
+            S.red[2][ty] = c_;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
-            float a = red[0][0], bb = red[1][0], c = red[2][0];
-            for (int i = 1; i < kWarps; ++i) {
-                a = fmaxf(a, red[0][i]);
-                bb = fmaxf(bb, red[1][i]);
-                c = fminf(c, red[2][i]);
+        if (tid == 0) {
+            float a = S.red[0][0], bb = S.red[1][0], c = S.red[2][0];
+            for (int w = 1; w < kWarps; ++w) {
+                a = fmaxf(a, S.red[0][w]);
+                bb = fmaxf(bb, S.red[1][w]);
+                c = fminf(c, S.red[2][w]);
             }
             atomicMax(mx + 4 * m + 0, __float_as_uint(a));
             atomicMax(mx + 4 * m + 1, __float_as_uint(bb));
@@ -313,16 +431,27 @@ void launch_q_half_apply(cudaStream_t s, const CUtensorMap* smap, const SweParam
                          const ErrParams& ep, const double* corr, const int* offsets,
                          double scale, float* eta, float* hu, float* hv, int* err,
                          int* err_pos, int M, unsigned* mx, const char* prof_name) {
-    dim3 grid((sp.nx + TX - 1) / TX, (sp.ny + TY - 1) / TY, M);
+    // strips of S tiles: long enough to amortise the strip prologue, short enough to keep
+    // >= ~8 waves of resident CTAs
+    const int tiles_x = (sp.nx + TX - 1) / TX, tiles_y = (sp.ny + TY - 1) / TY;
+    const double slots = 148.0 * DC_QHALF_MIN_BLOCKS;
+    int S = static_cast<int>(static_cast<double>(tiles_x) * tiles_y * M / (DC_QHALF_WAVES * slots));
+    S = S < 1 ? 1 : (S > tiles_y ? tiles_y : S);
+    const int strips = (tiles_y + S - 1) / S;
+    S = (tiles_y + strips - 1) / strips;  // balance the strips
+    dim3 grid(tiles_x, strips, M);
+    // < 48 KB for every c_omega (ring <= 37 rows): no opt-in
+    const size_t smem = sizeof(QhSmem) + static_cast<size_t>(qh_ring(ep.c)) * tile::XW * sizeof(double);
     // the state read and written once (24 B/cell) + the coarse field
     KScope ks(s, prof_name,
               (24.0 * sp.nx * sp.ny + 8.0 * ep.nxc * ep.nyc) * M);
-    if (scale == 1.0)
-        q_half_apply_kernel<true><<<grid, tile::NT, 0, s>>>(*smap, sp, ep, corr, offsets, scale,
-                                                            eta, hu, hv, err, err_pos, mx);
-    else
-        q_half_apply_kernel<false><<<grid, tile::NT, 0, s>>>(*smap, sp, ep, corr, offsets, scale, eta, hu,
-                                                  hv, err, err_pos, mx);
+    if (scale == 1.0) {
+        q_half_apply_kernel<true><<<grid, tile::NT, smem, s>>>(*smap, sp, ep, corr, offsets, scale,
+                                                            eta, hu, hv, err, err_pos, mx, S);
+    } else {
+        q_half_apply_kernel<false><<<grid, tile::NT, smem, s>>>(*smap, sp, ep, corr, offsets, scale,
+                                                             eta, hu, hv, err, err_pos, mx, S);
+    }
 }
 
 } // namespace dcg
