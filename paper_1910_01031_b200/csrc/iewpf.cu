@@ -427,8 +427,13 @@ pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrPar
     if (P.T[0].ns > 0) pull_pass1(P.T[0], P.W[0], P.X);
     __syncthreads();
     if (P.T[0].nh > 0) pull_pass2(P.T[0], P.X, P.D0);
-    bool dry = false;
-    int dry_at = 0x7fffffff;
+    bool dryq[kRowsPerThread], rowok[kRowsPerThread];
+#pragma unroll
+    for (int q = 0; q < kRowsPerThread; ++q) {
+        const int r = ty + kWarps * q;
+        dryq[q] = false;
+        rowok[q] = r < TY && k0 + r < sp.ny;
+    }
     const double cy = ep.cy, cx = ep.cx, heq = ep.h_eq;
     const bool colok = j < sp.nx;
     for (int li = 0; li < cnt; ++li) {
@@ -441,23 +446,21 @@ pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrPar
         // the float state unchanged)
         {
             const PullTab& T = P.T[li & 1];
-            const double(*D)[tile::XW] = (li & 1) ? P.u.D1 : P.D0;
+            // this thread's D entries: one base, rows kWarps apart (immediate offsets)
+            const double* Dc = ((li & 1) ? &P.u.D1[0][0] : &P.D0[0][0]) + (ty + 1) * tile::XW + tx + 1;
             const int ar0 = T.ar0, ar1 = T.ar1;
-            const int jl = tx + 1;
-            const bool colin = colok && jl >= T.ac0 && jl <= T.ac1;
+            const bool colin = colok && tx + 1 >= T.ac0 && tx + 1 <= T.ac1;
 #pragma unroll
             for (int q = 0; q < kRowsPerThread; ++q) {
-                const int r = ty + kWarps * q, rr = r + 1, k = k0 + r;
-                if (r >= TY || rr < ar0 || rr > ar1) continue;  // warp-uniform
-                if (!colin || k >= sp.ny) continue;
-                const double de = D[rr][jl];
-                const double dhu = -cy * (D[rr + 1][jl] - D[rr - 1][jl]);
-                const double dhv = cx * (D[rr][jl + 1] - D[rr][jl - 1]);
+                const int rr = ty + 1 + kWarps * q;
+                if (!rowok[q] || rr < ar0 || rr > ar1) continue;  // warp-uniform
+                if (!colin) continue;
+                const double* d = Dc + q * kWarps * tile::XW;
+                const double de = d[0];
+                const double dhu = -cy * (d[tile::XW] - d[-tile::XW]);
+                const double dhv = cx * (d[1] - d[-1]);
                 const double ee = static_cast<double>(se[q]) + 1.0 * de;
-                if (!(heq + ee > 0.0)) {
-                    dry = true;
-                    dry_at = min(dry_at, k * sp.nx + j);
-                }
+                dryq[q] |= !(heq + ee > 0.0);
                 se[q] = static_cast<float>(ee);
                 su[q] = static_cast<float>(static_cast<double>(su[q]) + 1.0 * dhu);
                 sv[q] = static_cast<float>(static_cast<double>(sv[q]) + 1.0 * dhv);
@@ -477,6 +480,14 @@ pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrPar
         hu[o] = su[q];
         hv[o] = sv[q];
     }
+    bool dry = false;
+    int dry_at = 0x7fffffff;
+#pragma unroll
+    for (int q = kRowsPerThread - 1; q >= 0; --q)
+        if (dryq[q]) {
+            dry = true;
+            dry_at = (k0 + ty + kWarps * q) * sp.nx + j;  // the thread's first dry cell
+        }
     if (dry) {
         atomicCAS(err + m, 0, E_DRY_ADD);
         atomicMin(err_pos + m, dry_at);
