@@ -177,6 +177,8 @@ void derive_params(dc_ctx* c) {
     P.idx = static_cast<float>(1.0 / g.dx);
     P.idy = static_cast<float>(1.0 / g.dy);
     P.fH = static_cast<float>(g.f / g.h_eq);
+    P.half_theta = 0.5f * P.theta;
+    P.fH_4 = 0.25f * P.fH;
     P.dx = g.dx;
     P.dy = g.dy;
     P.courant = g.courant;

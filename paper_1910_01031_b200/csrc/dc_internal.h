@@ -45,6 +45,7 @@ struct SweParams {
     int end_mode;         // stage 2: fused substep end (0 off, 1 flag only, 2 + graph cond)
     unsigned long long end_cond;  // cudaGraphConditionalHandle of the step's while node
     float H, g, theta, cf_x, cf_y, inv_g, idx, idy, fH;
+    float half_theta, fH_4;  // theta / 2, fH / 4 (exact scalings, swe.cu reconP / seg_tend)
     double dx, dy, courant, model_dt, h_eq, gd;
     float neg_zero;       // -0.0f, opaque to ptxas (packed-product addend, swe.cu)
 };
