@@ -210,102 +210,126 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
 
-// The interpolation tables of one (tile, covering observation) plus everything the pull
-// derives from the window's reach, precomputed so pull_apply's loop carries no searches or
-// divisions: the column groups pass 1 evaluates, the X slots pass 2 reads, the row groups
-// and columns pass 2 evaluates, and the box the add covers.
-struct alignas(16) PullTab : tile::Tab {
-    int g0, npg;          // pass 1: column groups g0 .. g0 + npg - 1
-    int ns;               // pass 1: X slots slot[0 .. ns-1] (the ones pass 2 reads)
-    int h0, nh, ca, w;    // pass 2: row groups h0 .. h0 + nh - 1 x halo columns ca .. ca + w - 1
-    int ar0, ar1, ac0, ac1;  // the add: halo rows ar0..ar1 x halo columns ac0..ac1
-    float inv_npg, inv_w;    // 1/npg, 1/w: exact flat-index splits (index < 2^11)
-    int slot[tile::NBMAX];
+// The interpolation tables of one (tile, covering observation) in the compact form the
+// pull reads (~1 KB), plus everything derived from the window's reach, precomputed so
+// pull_apply's loop carries no searches or divisions: the column groups pass 1 evaluates,
+// the coarse rows ("slots") pass 2 reads -- numbered compactly -- the row groups and
+// columns pass 2 evaluates, and the box the add covers.
+struct alignas(16) PullTab {
+    double ct[tile::XW];             // x fraction per halo column
+    double rt[tile::YH];             // y fraction per halo row
+    uint8_t cg_a[tile::XW][4];       // per column group: window columns of its 4 coarse points
+    uint8_t cg_first[tile::XW + 1];  // first halo column of each column group (+ end)
+    uint8_t rg_si[tile::YH][4];      // per row group: compact slots of its 4 coarse rows
+    uint8_t rg_first[tile::YH + 1];  // first halo row of each row group (+ end)
+    uint8_t wrow[tile::NBMAX + 1];   // window row of each compact slot
+    int ns, npg, g0;                 // pass 1: slots 0..ns-1 x column groups g0..g0+npg-1
+    int nh, h0, ca, w;               // pass 2: row groups h0..h0+nh-1 x halo columns ca..ca+w-1
+    int ar0, ar1, ac0, ac1;          // the add: halo rows ar0..ar1 x halo columns ac0..ac1
+    float inv_npg, inv_w;            // 1/npg, 1/w: exact flat-index splits (index < 2^11)
 };
 constexpr int kPullTabChunks = (sizeof(PullTab) + 15) / 16;
+// compact slots a tile can need: (row groups over 32 halo rows) + 3
+__host__ __device__ constexpr int pull_slots(int c) {
+    return 32 / c + 5 < tile::NBMAX + 1 ? 32 / c + 5 : tile::NBMAX + 1;
+}
 
 // Interpolation tables of every (tile, covering observation): they depend on the tile and
 // the observation's coarse alignment only, not on the particle, so they are built once per
 // analysis here instead of in every (particle, tile) CTA. One 96-thread CTA per entry
-// (warp 0 columns, warps 1-2 rows, as tile::setup).
+// (warp 0 columns, warps 1-2 rows, as tile::setup_cols / setup_rows) into shared memory,
+// then the compact table.
 __global__ void __launch_bounds__(96)
 pull_tables_kernel(SweParams sp, ErrParams ep, const int4* __restrict__ lists,
                    const int* __restrict__ counts, int n_obs, int tiles_x, PullTab* tabs) {
     const int tl = blockIdx.x, li = blockIdx.y;
     if (li >= counts[tl]) return;
+    __shared__ tile::Tab F;
+    __shared__ int map[tile::NBMAX];
     const int4 ent = lists[static_cast<size_t>(tl) * n_obs + li];
     const int oj = ent.y & 0xffff, ok = ent.y >> 16, ao = ent.z, bo = ent.w;
     const int j0 = (tl % tiles_x) * TX, k0 = (tl / tiles_x) * TY;
     const int nxc = ep.nxc, nyc = ep.nyc;
     PullTab& T = tabs[static_cast<size_t>(tl) * n_obs + li];
     // coarse indices -> the padded window (indices 11..15 read exact zeros)
-    tile::setup_cols(T, ep, sp.nx, j0, oj, [&](int a) {
+    tile::setup_cols(F, ep, sp.nx, j0, oj, [&](int a) {
         const int da = wrapf(a - ao + WH, nxc);
         return da < WIN ? da : WP - 1;
     });
-    tile::setup_rows(T, ep, sp.ny, k0, ok, [&](int b) {
+    tile::setup_rows(F, ep, sp.ny, k0, ok, [&](int b) {
         const int db = wrapf(b - bo + WH, nyc);
-        return (db < WIN ? db : WP - 1) * WP;
+        return db < WIN ? db : WP - 1;
     });
-    __syncthreads();  // the tables above are global memory written by warps 0-2
+    __syncthreads();
+    const int tid = threadIdx.x;
     // the window's reach inside the tile: column groups / row groups with at least one of
     // their four coarse points inside the 11x11 window (the others interpolate to exactly 0)
-    if (threadIdx.x < 32) {
-        const int l = threadIdx.x;
+    if (tid < 32) {
+        const int l = tid;
         bool ca_ = false, ra_ = false;
-        if (l < T.ncg)
-            for (int q = 0; q < 4; ++q) ca_ |= T.cg_a[l][q] != WP - 1;
-        if (l < T.nrg)
-            for (int q = 0; q < 4; ++q) ra_ |= T.brow[T.rg_sl[l][q]] != (WP - 1) * WP;
+        if (l < F.ncg)
+            for (int q = 0; q < 4; ++q) ca_ |= F.cg_a[l][q] != WP - 1;
+        if (l < F.nrg)
+            for (int q = 0; q < 4; ++q) ra_ |= F.brow[F.rg_sl[l][q]] != WP - 1;
         const unsigned bc = __ballot_sync(0xffffffffu, ca_), br = __ballot_sync(0xffffffffu, ra_);
         if (l == 0) {
             if (bc && br) {
-                const int gc0 = __ffs(bc) - 1, gc1 = 31 - __clz(bc);
-                const int gr0 = __ffs(br) - 1, gr1 = 31 - __clz(br);
-                T.c0 = T.cg_first[gc0];
-                T.c1 = T.cg_first[gc1 + 1] - 1;
-                T.r0 = T.rg_first[gr0];
-                T.r1 = T.rg_first[gr1 + 1] - 1;
+                const int c0 = F.cg_first[__ffs(bc) - 1], c1 = F.cg_first[32 - __clz(bc)] - 1;
+                const int r0 = F.rg_first[__ffs(br) - 1], r1 = F.rg_first[32 - __clz(br)] - 1;
                 // D is needed on the reach + 2 (the geostrophic differences of the cells
                 // next to it read one more D); the add covers the reach + 1
-                const int ra = max(T.r0 - 2, 0), rb = min(T.r1 + 2, tile::YH - 1);
-                const int ca = max(T.c0 - 2, 0), cb = min(T.c1 + 2, tile::XW - 1);
-                int g0 = 0, g1 = T.ncg - 1;
-                while (g0 < g1 && T.cg_first[g0 + 1] <= ca) ++g0;
-                while (g1 > g0 && T.cg_first[g1] > cb) --g1;
-                int h0 = 0, h1 = T.nrg - 1;
-                while (h0 < h1 && T.rg_first[h0 + 1] <= ra) ++h0;
-                while (h1 > h0 && T.rg_first[h1] > rb) --h1;
+                const int ra = max(r0 - 2, 0), rb = min(r1 + 2, tile::YH - 1);
+                const int ca = max(c0 - 2, 0), cb = min(c1 + 2, tile::XW - 1);
+                int g0 = 0, g1 = F.ncg - 1;
+                while (g0 < g1 && F.cg_first[g0 + 1] <= ca) ++g0;
+                while (g1 > g0 && F.cg_first[g1] > cb) --g1;
+                int h0 = 0, h1 = F.nrg - 1;
+                while (h0 < h1 && F.rg_first[h0 + 1] <= ra) ++h0;
+                while (h1 > h0 && F.rg_first[h1] > rb) --h1;
                 unsigned long long need = 0;
                 for (int g = h0; g <= h1; ++g)
-                    for (int q = 0; q < 4; ++q) need |= 1ull << T.rg_sl[g][q];
+                    for (int q = 0; q < 4; ++q) need |= 1ull << F.rg_sl[g][q];
                 int ns = 0;
-                for (int sl = 0; sl < T.nb; ++sl)
-                    if (need >> sl & 1ull) T.slot[ns++] = sl;
+                for (int sl = 0; sl < F.nb; ++sl) {
+                    map[sl] = ns;
+                    if (need >> sl & 1ull) T.wrow[ns++] = static_cast<uint8_t>(F.brow[sl]);
+                }
+                if (ns > pull_slots(ep.c)) __trap();  // the slot bound of the launcher
+                T.ns = ns;
                 T.g0 = g0;
                 T.npg = g1 - g0 + 1;
-                T.ns = ns;
                 T.h0 = h0;
                 T.nh = h1 - h0 + 1;
                 T.ca = ca;
                 T.w = cb - ca + 1;
-                T.ar0 = max(T.r0 - 1, 1);
-                T.ar1 = min(T.r1 + 1, TY);
-                T.ac0 = max(T.c0 - 1, 1);
-                T.ac1 = min(T.c1 + 1, TX);
+                T.ar0 = max(r0 - 1, 1);
+                T.ar1 = min(r1 + 1, TY);
+                T.ac0 = max(c0 - 1, 1);
+                T.ac1 = min(c1 + 1, TX);
                 T.inv_npg = 1.0f / static_cast<float>(T.npg);
                 T.inv_w = 1.0f / static_cast<float>(T.w);
             } else {
-                T.r0 = 1;
-                T.r1 = 0;
-                T.c0 = 1;
-                T.c1 = 0;
-                T.npg = T.ns = T.nh = T.w = 0;
+                T.ns = T.npg = T.nh = T.w = 0;
                 T.ar0 = 1;
                 T.ar1 = 0;
+                T.ac0 = 1;
+                T.ac1 = 0;
             }
         }
     }
+    __syncthreads();
+    // the compact arrays (entries past the used groups are never read)
+    for (int i = tid; i < tile::XW; i += 96) {
+        T.ct[i] = F.ct[i];
+        for (int q = 0; q < 4; ++q) T.cg_a[i][q] = static_cast<uint8_t>(F.cg_a[i][q]);
+    }
+    for (int i = tid; i <= tile::XW; i += 96) T.cg_first[i] = static_cast<uint8_t>(F.cg_first[min(i, F.ncg)]);
+    for (int i = tid; i < tile::YH; i += 96) {
+        T.rt[i] = F.rt[i];
+        if (i < F.nrg)
+            for (int q = 0; q < 4; ++q) T.rg_si[i][q] = static_cast<uint8_t>(map[F.rg_sl[i][q]]);
+    }
+    for (int i = tid; i <= tile::YH; i += 96) T.rg_first[i] = static_cast<uint8_t>(F.rg_first[min(i, F.nrg)]);
 }
 
 constexpr int kStw = TX + 4;  // TMA box width: cells j0-2 .. j0+TX+1 (16-byte aligned start)
@@ -316,21 +340,20 @@ __device__ __forceinline__ int div_small(int i, float inv_n) {
     return __float2int_rz(__fmul_rn(static_cast<float>(i) + 0.5f, inv_n));
 }
 
-// pass 1 of one entry (the observation's window W through its tables T): X for the needed
-// slots x the column groups of the reach (interp_tile.cuh: one Catmull-Rom coefficient set
-// per (slot, group), the t-polynomial per fine column)
+// pass 1 of one entry (the observation's window W through its tables T): X for the
+// entry's slots x the column groups of the reach (interp_tile.cuh: one Catmull-Rom
+// coefficient set per (slot, group), the t-polynomial per fine column)
 __device__ __forceinline__ void pull_pass1(const PullTab& T, const double* __restrict__ W,
                                            double (*X)[tile::XW]) {
     const int n = T.ns * T.npg;
     for (int i = threadIdx.x; i < n; i += tile::NT) {
         const int si = div_small(i, T.inv_npg);
         const int g = T.g0 + (i - si * T.npg);
-        const int s = T.slot[si];
-        const double* wr = W + T.brow[s];
+        const double* wr = W + T.wrow[si] * WP;
         const tile::Cm m = tile::coef(wr[T.cg_a[g][0]], wr[T.cg_a[g][1]], wr[T.cg_a[g][2]],
                                       wr[T.cg_a[g][3]]);
         const int j1 = T.cg_first[g + 1];
-        for (int jl = T.cg_first[g]; jl < j1; ++jl) X[s][jl] = tile::eval(m, T.ct[jl]);
+        for (int jl = T.cg_first[g]; jl < j1; ++jl) X[si][jl] = tile::eval(m, T.ct[jl]);
     }
 }
 
@@ -341,8 +364,8 @@ __device__ __forceinline__ void pull_pass2(const PullTab& T, const double (*X)[t
     for (int i = threadIdx.x; i < n; i += tile::NT) {
         const int gi = div_small(i, T.inv_w);
         const int g = T.h0 + gi, jl = T.ca + (i - gi * T.w);
-        const tile::Cm m = tile::coef(X[T.rg_sl[g][0]][jl], X[T.rg_sl[g][1]][jl],
-                                      X[T.rg_sl[g][2]][jl], X[T.rg_sl[g][3]][jl]);
+        const tile::Cm m = tile::coef(X[T.rg_si[g][0]][jl], X[T.rg_si[g][1]][jl],
+                                      X[T.rg_si[g][2]][jl], X[T.rg_si[g][3]][jl]);
         const int r1 = T.rg_first[g + 1];
         for (int r = T.rg_first[g]; r < r1; ++r) D[r][jl] = tile::eval(m, T.rt[r]);
     }
@@ -352,20 +375,24 @@ __device__ __forceinline__ void pull_pass2(const PullTab& T, const double (*X)[t
 // particle (optimal_proposal_pull, SPEC.md:455-463 + add_q_half, stochastic.hpp:144-160):
 // each thread keeps its cells' state in registers across all of the tile's observations
 // and adds them in ascending id, rounding to float after every add as the reference's
-// per-observation add_q_half does. The observations run as a two-barrier software
-// pipeline: while entry i is added from its D, entry i+1's pass 1 fills X; then entry
-// i+1's pass 2 fills the other D while entry i+2's window and tables stream in.
+// per-observation add_q_half does. The observations run as a three-stage software
+// pipeline with one barrier per observation: in the segment of entry i, entry i+2's
+// pass 1 fills one X, entry i+1's pass 2 reads the other X into one D, entry i is added
+// from the other D, and entry i+3's window and tables stream into the fourth buffer.
 struct PullSmem {
     union alignas(128) {  // the TMA box of the tile's state (128-byte aligned), then (once
         float ST[3][TY][kStw];  // in registers) the second D
         double D1[tile::YH][tile::XW];
     } u;
-    double W[2][WP * WP];
-    PullTab T[2];
-    double X[tile::NBMAX][tile::XW];
     double D0[tile::YH][tile::XW];
+    double W[4][WP * WP];
+    PullTab T[4];
     unsigned long long bar;
+    // then X[2][slots][XW] doubles (dynamic, pull_slots(c) rows each)
 };
+size_t pull_smem_bytes(int c) {
+    return (sizeof(PullSmem) + 7) / 8 * 8 + 2ull * pull_slots(c) * tile::XW * sizeof(double);
+}
 
 __global__ void __launch_bounds__(tile::NT, DC_PULL_MIN_BLOCKS)
 pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrParams ep,
@@ -373,7 +400,12 @@ pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrPar
                   const int4* __restrict__ lists, const int* __restrict__ counts, int tiles_x,
                   const PullTab* __restrict__ tabs, float* eta, float* hu, float* hv,
                   int* err, int* err_pos) {
-    __shared__ alignas(128) PullSmem P;
+    extern __shared__ __align__(128) unsigned char pull_raw[];
+    PullSmem& P = *reinterpret_cast<PullSmem*>(pull_raw);
+    const int xr = pull_slots(ep.c);
+    double(*X0)[tile::XW] =
+        reinterpret_cast<double(*)[tile::XW]>(pull_raw + (sizeof(PullSmem) + 7) / 8 * 8);
+    double(*X1)[tile::XW] = X0 + xr;
     const int m = blockIdx.y;
     // another tile of the member may raise E_DRY_ADD meanwhile: decide once per CTA
     if (__syncthreads_or(err[m] != 0)) return;
@@ -391,25 +423,28 @@ pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrPar
         tma_row(smem_u32(&P.u.ST[0][0][0]), &smap, j0, m * (sp.ny + 4) + 2 + k0, b);
     }
     // the windows' pad (da or db >= WIN) stays zero; the copies touch only da, db < WIN
-    for (int i = tid; i < 2 * WP * WP; i += tile::NT) {
+    for (int i = tid; i < 4 * WP * WP; i += tile::NT) {
         const int e = i & (WP * WP - 1);
         if ((e & (WP - 1)) >= WIN || (e >> 4) >= WIN) P.W[i >> 8][e] = 0.0;
     }
     const int4* tlist = lists + static_cast<size_t>(tl) * n_obs;
     const PullTab* ttab = tabs + static_cast<size_t>(tl) * n_obs;
     const double* wbase = win + static_cast<size_t>(m) * n_obs * (WIN * WIN);
-    auto load = [&](int li) {  // entry li's 11x11 window and tables into buffer li & 1
-        const int q = li & 1;
-        if (tid < WIN * WIN)
-            cp_async8d(&P.W[q][(tid / WIN) * WP + tid % WIN],
-                       wbase + static_cast<size_t>(tlist[li].x) * (WIN * WIN) + tid);
-        for (int c = tid; c < kPullTabChunks; c += tile::NT)
-            cp_async16(reinterpret_cast<char*>(&P.T[q]) + 16 * c,
-                       reinterpret_cast<const char*>(ttab + li) + 16 * c);
-        asm volatile("cp.async.commit_group;\n" ::);
+    auto load = [&](int li) {  // entry li's 11x11 window and tables into buffer li & 3
+        const int q = li & 3;
+        if (li < cnt) {
+            if (tid < WIN * WIN)
+                cp_async8d(&P.W[q][(tid / WIN) * WP + tid % WIN],
+                           wbase + static_cast<size_t>(tlist[li].x) * (WIN * WIN) + tid);
+            for (int c = tid; c < kPullTabChunks; c += tile::NT)
+                cp_async16(reinterpret_cast<char*>(&P.T[q]) + 16 * c,
+                           reinterpret_cast<const char*>(ttab + li) + 16 * c);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);  // (empty past the list: uniform counts)
     };
     load(0);
-    if (cnt > 1) load(1);
+    load(1);
+    load(2);
     // the thread's cells: halo row ty + 1 + kWarps q, halo column tx + 1
     float se[kRowsPerThread], su[kRowsPerThread], sv[kRowsPerThread];
     __syncthreads();  // the mbarrier is initialised
@@ -421,12 +456,13 @@ pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrPar
         su[q] = P.u.ST[1][r][tx + 2];
         sv[q] = P.u.ST[2][r][tx + 2];
     }
-    if (cnt > 1) asm volatile("cp.async.wait_group 1;\n" ::);
-    else asm volatile("cp.async.wait_group 0;\n" ::);
+    asm volatile("cp.async.wait_group 2;\n" ::);
     __syncthreads();  // entry 0 landed; the state box is in registers (D1 may be written)
-    if (P.T[0].ns > 0) pull_pass1(P.T[0], P.W[0], P.X);
-    __syncthreads();
-    if (P.T[0].nh > 0) pull_pass2(P.T[0], P.X, P.D0);
+    pull_pass1(P.T[0], P.W[0], X0);
+    asm volatile("cp.async.wait_group 1;\n" ::);
+    __syncthreads();  // X of entry 0 complete; entry 1 landed
+    if (cnt > 1) pull_pass1(P.T[1], P.W[1], X1);
+    pull_pass2(P.T[0], X0, P.D0);
     bool dryq[kRowsPerThread], rowok[kRowsPerThread];
 #pragma unroll
     for (int q = 0; q < kRowsPerThread; ++q) {
@@ -438,14 +474,14 @@ pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrPar
     const bool colok = j < sp.nx;
     for (int li = 0; li < cnt; ++li) {
         asm volatile("cp.async.wait_group 0;\n" ::);
-        __syncthreads();  // D of entry li complete, X free, entry li+1 landed
-        const bool more = li + 1 < cnt;
-        const PullTab& Tn = P.T[(li + 1) & 1];
-        if (more && Tn.ns > 0) pull_pass1(Tn, P.W[(li + 1) & 1], P.X);
+        __syncthreads();  // D of entry li, X of entry li+1 complete; entry li+2 landed
+        if (li + 2 < cnt) pull_pass1(P.T[(li + 2) & 3], P.W[(li + 2) & 3], (li & 1) ? X1 : X0);
+        if (li + 1 < cnt)
+            pull_pass2(P.T[(li + 1) & 3], (li & 1) ? X0 : X1, (li & 1) ? P.D0 : P.u.D1);
         // entry li's add on its box (outside it the pull is an exact zero, whose add leaves
         // the float state unchanged)
         {
-            const PullTab& T = P.T[li & 1];
+            const PullTab& T = P.T[li & 3];
             // this thread's D entries: one base, rows kWarps apart (immediate offsets)
             const double* Dc = ((li & 1) ? &P.u.D1[0][0] : &P.D0[0][0]) + (ty + 1) * tile::XW + tx + 1;
             const int ar0 = T.ar0, ar1 = T.ar1;
@@ -466,9 +502,7 @@ pull_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrPar
                 sv[q] = static_cast<float>(static_cast<double>(sv[q]) + 1.0 * dhv);
             }
         }
-        __syncthreads();  // X complete; entry li's window, tables and D are free
-        if (li + 2 < cnt) load(li + 2);
-        if (more && Tn.nh > 0) pull_pass2(Tn, P.X, (li & 1) ? P.D0 : P.u.D1);
+        load(li + 3);  // into the buffer entry li-1 used (its add ended before the barrier)
     }
     const size_t mbase = static_cast<size_t>(m) * sp.mstride;
 #pragma unroll
@@ -845,7 +879,9 @@ void launch_pull_apply(cudaStream_t s, const CUtensorMap* smap, const SweParams&
     // window once, the tables once
     KScope ks(s, "pull_apply", (24.0 * touched_cells + 8.0 * WIN * WIN * n_obs) * M +
                                    entries * sizeof(PullTab));
-    pull_apply_kernel<<<dim3(n_tiles, M), tile::NT, 0, s>>>(*smap, sp, ep, win, n_obs,
+    const size_t smem = pull_smem_bytes(ep.c);
+    smem_opt_in(pull_apply_kernel, pull_smem_bytes(1));  // the largest (c_omega = 1)
+    pull_apply_kernel<<<dim3(n_tiles, M), tile::NT, smem, s>>>(*smap, sp, ep, win, n_obs,
                                                        reinterpret_cast<const int4*>(lists), counts,
                                                        tiles_x, T, eta, hu, hv, err, err_pos);
 }
