@@ -346,7 +346,9 @@ __device__ __forceinline__ int div_small(int i, float inv_n) {
 __device__ __forceinline__ void pull_pass1(const PullTab& T, const double* __restrict__ W,
                                            double (*X)[tile::XW]) {
     const int n = T.ns * T.npg;
-    for (int i = threadIdx.x; i < n; i += tile::NT) {
+    // from the last thread down: the segment's add gives the last two warps one row fewer
+    // (30 rows over 8 warps), so pass 1 (~2.5 rows' worth per item) goes there first
+    for (int i = tile::NT - 1 - threadIdx.x; i < n; i += tile::NT) {
         const int si = div_small(i, T.inv_npg);
         const int g = T.g0 + (i - si * T.npg);
         const double* wr = W + T.wrow[si] * WP;
