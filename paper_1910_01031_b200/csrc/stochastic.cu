@@ -179,7 +179,7 @@ struct QhSmem {
     float ST[3][TY][kStw];       // the tile's state box (TMA), 128-byte aligned at offset 0
     double D[2][tile::YH][tile::XW];
     QhCols C;
-    QhRows R[2];
+    QhRows R[3];  // tile i in R[i % 3]
     float red[3][kWarps];
     unsigned long long bar;
     // then X[ring][XW] doubles (dynamic)
@@ -224,7 +224,8 @@ __device__ __forceinline__ void qh_xpass(const QhCols& C, const ErrParams& ep,
                                          int ring, int u0, int u1) {
     const int ncg = C.ncg, n = (u1 - u0 + 1) * ncg;
     const float inv_ncg = 1.0f / static_cast<float>(ncg);
-    for (int i = threadIdx.x; i < n; i += tile::NT) {
+    // from the last thread down: the add gives the last two warps one row fewer
+    for (int i = tile::NT - 1 - threadIdx.x; i < n; i += tile::NT) {
         const int ui = __float2int_rz(__fmul_rn(static_cast<float>(i) + 0.5f, inv_ncg));
         const int g = i - ui * ncg;
         const int u = u0 + ui;
@@ -286,10 +287,10 @@ q_half_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrP
         tma_row(smem_u32(&S.ST[0][0][0]), &smap, j0, m * (sp.ny + 4) + 2 + t0 * TY, b);
     }
     tile::setup_cols(S.C, ep, sp.nx, j0, oj, [](int a) { return a; });
-    if (warp == 1) qh_rows(S.R[0], ep, sp.ny, t0 * TY, ok, ring);
+    if (warp == kWarps - 1) qh_rows(S.R[0], ep, sp.ny, t0 * TY, ok, ring);
     __syncthreads();
     qh_xpass(S.C, ep, cf, X, ring, S.R[0].rg_u[0] - 1, S.R[0].u_last);
-    if (warp == 1 && nt > 1) qh_rows(S.R[1], ep, sp.ny, (t0 + 1) * TY, ok, ring);
+    if (warp == 0 && nt > 1) qh_rows(S.R[1], ep, sp.ny, (t0 + 1) * TY, ok, ring);
     __syncthreads();
     qh_ypass(S.R[0], X, S.D[0]);
     bool dry = false;
@@ -299,7 +300,9 @@ q_half_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrP
     for (int i = 0; i < nt; ++i) {
         __syncthreads();  // D of tile i complete; tile i+1's row tables published
         const int k0 = (t0 + i) * TY;
-        if (i + 1 < nt) qh_xpass(S.C, ep, cf, X, ring, S.R[i & 1].u_last + 1, S.R[(i + 1) & 1].u_last);
+        if (i + 1 < nt) qh_xpass(S.C, ep, cf, X, ring, S.R[i % 3].u_last + 1, S.R[(i + 1) % 3].u_last);
+        // tile i+2's row tables (into the buffer tile i-1 used) on a warp with one row fewer
+        if (warp == kWarps - 1 && i + 2 < nt) qh_rows(S.R[(i + 2) % 3], ep, sp.ny, k0 + 2 * TY, ok, ring);
         // geostrophic balance (stochastic.hpp:122-139) + add in fp64, cast to float
         mbar_wait(b, i & 1);
         const double(*D)[tile::XW] = S.D[i & 1];
@@ -364,8 +367,7 @@ q_half_apply_kernel(const __grid_constant__ CUtensorMap smap, SweParams sp, ErrP
                 mbar_expect_tx(b, sizeof(S.ST));
                 tma_row(smem_u32(&S.ST[0][0][0]), &smap, j0, m * (sp.ny + 4) + 2 + k0 + TY, b);
             }
-            if (warp == 1 && i + 2 < nt) qh_rows(S.R[i & 1], ep, sp.ny, k0 + 2 * TY, ok, ring);
-            qh_ypass(S.R[(i + 1) & 1], X, S.D[(i + 1) & 1]);
+            qh_ypass(S.R[(i + 1) % 3], X, S.D[(i + 1) & 1]);
         }
     }
     if (dry) {
