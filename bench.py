@@ -190,10 +190,12 @@ def load_peaks():
 
 
 # FP32 lane operations per cell of the exact stage kernels: predicated-on FFMA2/FADD2/FMUL2
-# (2 each) + FFMA/FADD/FMUL (1) executed per member cell in the ncu source page of
-# profiles/r2_swe_stage_ncu.json (215.6 / 238.1 at 1000x600), less the 256-for-252-column
-# window halo (x 1000/1024): the work one output cell needs. Stage 1, stage 2.
-FP32_OPS_PER_CELL = (210.5, 232.5)
+# (2 each) + FFMA/FADD/FMUL (1) executed per member cell in the ncu source page of the
+# final round-2 build's capture (profiles/r2_swe_stage_ncu.json: 201.8 / 224.0 at
+# 1000x600), less the 256-for-252-column window halo (x 1000/1024): the work one output
+# cell needs. Stage 1, stage 2. (The power-of-two folds and the carried y slopes removed
+# ~6 % of them: 210.5 / 232.5 before.)
+FP32_OPS_PER_CELL = (197.1, 218.7)
 
 # cycle stages ("stage shares") of every kernel name the profiler reports
 STAGE_OF = {

@@ -117,19 +117,22 @@ __global__ void pull_windows_kernel(ErrParams ep, const double* __restrict__ sd,
     const double vS = 0.0 + (ep.cyc * yhu);   // (a, b-1)
     const double vE = 0.0 + (ep.cxc * yhv);   // (a+1, b)
     const double vW = 0.0 + (-ep.cxc * yhv);  // (a-1, b)
+    // the first SOAR sees four non-zero inputs: its 25-term sum (db outer, da inner, from
+    // 0.0) is the sum of the (at most four) dipole terms in that order -- S (db = -1-pb),
+    // W and E (db = -pb), N (db = 1-pb) -- because the other terms add w * (+0) = +-0 to a
+    // partial sum that is never -0 (the dipole values are 0.0 + x, never -0; a sum that
+    // cancels is +0 under round-to-nearest), which leaves it unchanged
+    auto term = [&](int da, int db, double v, double s) {
+        return (da >= -2 && da <= 2 && db >= -2 && db <= 2) ? s + ep.w[(db + 2) * 5 + (da + 2)] * v
+                                                            : s;
+    };
     for (int i = threadIdx.x; i < WIN * WIN; i += blockDim.x) {
         const int pa = i % WIN - WH, pb = i / WIN - WH;  // offset from the obs point
         double s = 0.0;
-        for (int db = -2; db <= 2; ++db)
-            for (int da = -2; da <= 2; ++da) {
-                const int ra = pa + da, rb = pb + db;
-                double v = 0.0;
-                if (ra == 0 && rb == 1) v = vN;
-                else if (ra == 0 && rb == -1) v = vS;
-                else if (ra == 1 && rb == 0) v = vE;
-                else if (ra == -1 && rb == 0) v = vW;
-                s += ep.w[(db + 2) * 5 + (da + 2)] * v;
-            }
+        s = term(-pa, -1 - pb, vS, s);
+        s = term(-1 - pa, -pb, vW, s);
+        s = term(1 - pa, -pb, vE, s);
+        s = term(-pa, 1 - pb, vN, s);
         s1[i] = s;
     }
     __syncthreads();
