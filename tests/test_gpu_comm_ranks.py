@@ -70,7 +70,9 @@ print(json.dumps({"ranks": out, "one": one[0]}))
 '''
 
 
-@pytest.mark.parametrize("parts", [[3, 3], [2, 2, 3]])
+# [3, 3], [2, 2, 3]: even / uneven slices; the eight-rank partition of configs[3]
+# (1000 members over 8 GPUs), scaled down, with uneven slices
+@pytest.mark.parametrize("parts", [[3, 3], [2, 2, 3], [2, 1, 2, 2, 1, 2, 2, 2]])
 def test_comm_ranks_on_one_gpu_equal_one_context(tmp_path, parts):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
