@@ -256,6 +256,28 @@ def test_perturb_philox_bitwise(oracle):
         ens.close()
 
 
+@pytest.mark.parametrize("nx,ny,c,n", [(100, 305, 5, 1500), (99, 300, 3, 1500), (60, 90, 1, 4000)])
+def test_perturb_column_strips_bitwise(oracle, nx, ny, c, n):
+    """Enough members that q_half_apply runs as column strips of several tiles per CTA
+    (the coarse-row ring, the pipeline across tiles, the TMA box re-armed per tile, a
+    partial last tile at ny = 305; c_omega 5 / 3 / 1 size the ring): members at the start,
+    middle and end of the ensemble bitwise equal to the CPU restatement, two draws."""
+    _, Ensemble = _gpu()
+    cfg, p = cfg_pair(nx, ny, c_omega=c)
+    ens = Ensemble(cfg, n, member_base=3)
+    ens.init_double_jet()
+    for _ in range(2):
+        ens.perturb_state()
+    for m in (0, n // 2 + 1, n - 1):
+        s = oracle.init_double_jet(p)
+        for d in range(2):
+            oracle.perturb_philox(p, s, 3 + m, d)
+        e, u, v, _ = ens.download_member(m)
+        assert np.array_equal(e, s.eta), (nx, c, m)
+        assert np.array_equal(u, s.hu) and np.array_equal(v, s.hv), (nx, c, m)
+    ens.close()
+
+
 def test_step_perturb_sequence_bitwise(oracle):
     """Forecast with model error, 5 model steps with a Philox draw after each of the
     first 4 (the DA-cycle forecast pattern), bitwise."""
