@@ -1,6 +1,8 @@
-// interp_tile.cuh -- Catmull-Rom interpolation of a coarse field onto one 32x30 fine tile
-// (+1-cell halo) in shared memory, shared by q_half_apply (model error / posterior) and
-// pull_apply (IEWPF pull). Included only by --fmad=false translation units.
+// interp_tile.cuh -- the pieces of the Catmull-Rom interpolation of a coarse field onto a
+// 32x30 fine tile (+1-cell halo) shared by q_half_apply (stochastic.cu: column strips) and
+// the IEWPF pull (iewpf.cu: pull_tables / pull_apply): the tile geometry, the column /
+// row group tables and the Catmull-Rom coefficients. Included only by --fmad=false
+// translation units.
 //
 // interpolate_bicubic (stochastic.hpp:93-118) computes, per fine cell, four x-direction
 // Catmull-Rom evaluations col[m] (one per coarse row bs[m]) and one y-direction
@@ -29,11 +31,11 @@ constexpr int YH = TY + 2;         // tile height incl. halo (= 32: one lane per
 #define DC_TILE_NT 256
 #endif
 constexpr int NT = DC_TILE_NT;     // threads (a multiple of 32, >= 96)
-constexpr int kWarps = NT / 32;    // warps; the apply phase gives warp w rows w, w + kWarps, ..
+constexpr int kWarps = NT / 32;    // warps; an add gives warp w rows w, w + kWarps, ..
 constexpr int kRowsPerThread = (TY + kWarps - 1) / kWarps;
 
-// the interpolation tables of one (tile, coarse alignment): member-independent for the
-// IEWPF pull, so pull_apply reads them precomputed (pull_tables_kernel)
+// the interpolation tables of one (tile, coarse alignment) as setup_cols / setup_rows
+// build them (pull_tables_kernel compacts them into the pull's per-entry PullTab)
 struct Tab {
     double ct[XW];           // x fraction per halo column
     double rt[YH];           // y fraction per halo row
@@ -43,10 +45,6 @@ struct Tab {
     int rg_first[YH + 1];    // first halo row of each row group (+ end sentinel)
     int brow[NBMAX];         // coarse row of each X slot (mapped)
     int nb, ncg, nrg;
-    // IEWPF pull only (pull_tables): halo rows / columns where the interpolated field can be
-    // non-zero (the observation's 11x11 window reaches them), [r0, r1] x [c0, c1]; r0 > r1
-    // when the tile is outside the window's reach
-    int r0, r1, c0, c1;
 };
 struct Cm {
     double a, b, c, d;
