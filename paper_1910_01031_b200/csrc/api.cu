@@ -441,7 +441,7 @@ dc_status dc_create(const dc_config* cfg, int32_t n_members, int64_t member_base
 // 120-row strips; 125 members 19.90 / 19.67 / 19.57 at 40 / 86 / 120; at 500x300 x 100
 // members 28 rows stays best (86: +14 %, 120: +28 %: too few CTAs to fill the waves).
 static void choose_strips(SweParams& P, int sms, int per_sm) {
-    const int xt = (P.nx + 251) / 252;
+    const int xt = (P.nx + kSweOut - 1) / kSweOut;
     const double slots = static_cast<double>(sms) * per_sm;
     double best = 1e30;
     for (int s = std::max(1, (P.ny + 255) / 256); s <= std::max(1, (P.ny + 7) / 8); ++s) {
@@ -493,7 +493,7 @@ static dc_status dc_create_device(dc_ctx* ctx, int32_t device, void* stream) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
         const int per_sm = swe_stage_occupancy();
         choose_strips(ctx->sp, sms, per_sm);
-        stage_waves = static_cast<double>((ctx->sp.nx + 251) / 252) * ctx->M * ctx->sp.strips /
+        stage_waves = static_cast<double>((ctx->sp.nx + kSweOut - 1) / kSweOut) * ctx->M * ctx->sp.strips /
                       (static_cast<double>(sms) * per_sm);
     }
     // per-member kernels put the member index in gridDim.y / z (<= 65535)

@@ -29,6 +29,13 @@ enum DevErr : int {
 
 // Constants of the shallow-water stencil, derived exactly as the reference's Stepper
 // derives them (double, then one rounding to float): swe.hpp:277-278,340-344,356-357,380-382.
+// the stage kernel's column window: 2 columns per thread, a 2-column halo on each side
+#ifndef DC_SWE_COLS
+#define DC_SWE_COLS 256
+#endif
+constexpr int kSweCols = DC_SWE_COLS;
+constexpr int kSweOut = kSweCols - 4;
+
 struct SweParams {
     // state layout: every member holds (ny+4) x pitch floats per field -- the ny x nx
     // cells inside a 2-cell periodic ghost frame (stage kernels read it through TMA);
