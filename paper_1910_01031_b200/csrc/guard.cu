@@ -53,11 +53,14 @@ cudaError_t dmalloc_impl(void** p, size_t bytes, const char* file, int line) {
     cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&base), bytes + 2 * kGuard);
     if (e != cudaSuccess) return e;
     // the fills run on the legacy stream, which the library's non-blocking streams do not
-    // wait for: finish them before any stream can touch the buffer
-    if ((e = cudaMemset(base, kPattern, kGuard)) != cudaSuccess) return e;
-    if ((e = cudaMemset(base + kGuard, 0xFF, bytes)) != cudaSuccess) return e;
-    if ((e = cudaMemset(base + kGuard + bytes, kPattern, kGuard)) != cudaSuccess) return e;
-    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return e;
+    // wait for: finish them before any stream can touch the buffer -- by synchronising that
+    // stream only (a device-wide synchronisation would also wait for other contexts' work,
+    // which in a multi-rank process may be waiting for this rank's collective)
+    if ((e = cudaMemsetAsync(base, kPattern, kGuard, cudaStreamLegacy)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(base + kGuard, 0xFF, bytes, cudaStreamLegacy)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(base + kGuard + bytes, kPattern, kGuard, cudaStreamLegacy)) != cudaSuccess)
+        return e;
+    if ((e = cudaStreamSynchronize(cudaStreamLegacy)) != cudaSuccess) return e;
     char* user = base + kGuard;
     std::lock_guard<std::mutex> lk(g_mu);
     registry()[user] = Alloc{bytes, file, line};
